@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark of the FMM-BEM hot path (BASELINE.json metric) -- one JSON line on rank 0.
+
+Workload (BASELINE config 5): 10x10x10 randomly rotated copies of the
+synthetic lysozyme (C3: 102,152 panels, 2,000 atoms each) -> 102,152,000 panels,
+2,000,000 charges, eps 4/80, P = 10 terms, centroid rule.  A step is one application of
+the GMRES operator A = I - f K' (one "FMM evaluation" = one BEM iteration):
+upward sweep, M2L, downward sweep, P2P, L2P, all in libfmmbem's kernels, inputs resident
+in HBM.  x (409 MB) and the point data (3.3 GB) exceed the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c3|...] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_INTERACTION = 19.0  # SURVEY 8(d) convention for a K' interaction
+METRIC = "FMM-BEM matvec s and P2P Ginteractions/s at 1/2/4/8 B200; % FP32 peak"
+
+
+def fp32_peak_tflops(sm_count=148, mhz=1965.0):
+    """148 SMs x 128 FP32 lanes x 2 flops (FFMA) x max SM clock (B200_PROFILING.md / DESIGN.md)."""
+    return sm_count * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def workload(name):
+    from synth import configs
+    if name == "c5":
+        base = configs.lysozyme(113)
+        return configs.array((10, 10, 10), base=base), "array_10x10x10_lysozyme_nu113"
+    if name == "c5_small":  # 3x3x3 array (2.76 M panels)
+        base = configs.lysozyme(113)
+        return configs.array((3, 3, 3), base=base), "array_3x3x3_lysozyme_nu113"
+    if name == "c3":
+        return configs.lysozyme(113), "lysozyme_nu113"
+    if name == "c2":
+        return configs.kirkwood(64), "kirkwood_octa64"
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_sample(cfg, rows, x_global):
+    """FP64 oracle K' rows (plain direct sums over ALL sources) for a bounded target sample."""
+    from oracle import bem, _cdirect
+    pan = bem.Panels(cfg["vertices"], cfg["triangles"])
+    t0 = time.perf_counter()
+    y = bem.apply_kprime(pan, x_global, rows=rows)
+    dt = time.perf_counter() - t0
+    return y, dt, _cdirect.threads(), pan
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the FP64 oracle as it stands, on a bounded sample, rank 0 only."""
+    if rank != 0:
+        return
+    cfg, wname = workload(args.config)
+    n = len(cfg["triangles"])
+    rng = np.random.default_rng(7)
+    x = rng.normal(size=n)
+    rows_per_step = max(1, int(args.ref_rows))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, rng.choice(n, rows_per_step, replace=False), x)
+    times = []
+    for _ in range(args.steps):
+        _, dt, cores, _ = oracle_sample(cfg, rng.choice(n, rows_per_step, replace=False), x)
+        times.append(dt)
+    t_row = float(np.mean(times)) / rows_per_step
+    t_full = t_row * n  # extrapolated full direct matvec
+    value = 1.0 / t_full
+    sample = f"{rows_per_step} target rows x {n} sources per step (FP64 direct), extrapolated to {n} rows"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wname, "n_panels": n, "terms": args.terms, "quad_points": 1,
+                       "l2_flush": "inputs larger than L2"},
+            "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--terms", type=int, default=10)
+    ap.add_argument("--leaf-points", type=int, default=64)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--cpu-rows", type=int, default=128, help="oracle sample rows for cpu_baseline/parity")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1007_4591_b200 import Solver
+
+    cfg, wname = workload(args.config)
+    n = len(cfg["triangles"])
+    if world > 1:
+        # replicas: each rank runs the full problem on its own GPU
+        pass
+    t0 = time.perf_counter()
+    s = Solver.from_config(cfg, terms=args.terms, leaf_points=args.leaf_points, device=local)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    info = s.tree_info()
+    rng = np.random.default_rng(7)
+    x_global = rng.normal(size=n)
+    x = torch.tensor(s.to_local(x_global), dtype=torch.float32, device=f"cuda:{local}")
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        s.matvec(x, "A", out=y)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    phases = {k: [] for k in ("upward", "m2l", "p2p", "l2p", "total")}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+        tm = s.timing()  # per-phase CUDA-event times of this matvec (launch stream)
+        for k in phases:
+            phases[k].append(tm[k])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    tm = s.timing()
+    ph = {k: float(np.mean(v)) for k, v in phases.items()}
+    value = world / (ms * 1e-3) if dist else 1.0 / (ms * 1e-3)
+
+    # e2e: through the C ABI with pinned host buffers (H2D x, matvec, D2H y inside the region)
+    xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    xh.copy_(torch.from_numpy(s.to_local(x_global).astype(np.float32)))
+    yh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    xh_np, yh_np = xh.numpy(), yh.numpy()
+    for _ in range(2):
+        s.matvec_host(xh_np, "A", yh_np)
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        s.matvec_host(xh_np, "A", yh_np)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+
+    # BIBEE energy (charge-FMM + reduction), once, outside the timed region
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    bib = s.bibee("cfa")
+    bibee_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s.bibee("cfa")
+    bibee_warm_s = time.perf_counter() - t0
+
+    p2p_int = int(tm["p2p_interactions"])
+    p2p_s = ph["p2p"] * 1e-3
+    p2p_tflops = FLOPS_PER_INTERACTION * p2p_int / p2p_s / 1e12
+    peak = fp32_peak_tflops()
+    m2l_pairs = int(tm["m2l_pairs"])
+    P = args.terms
+    m2l_flops = 8.0 * (P * (P + 1) // 2) * P * P * m2l_pairs  # O(P^4) complex MACs per pair
+    dominant = max(("p2p", "m2l"), key=lambda k: ph[k])
+    if dominant == "p2p":
+        roof = {"kernel": "k_p2p (near field)", "bound": "alu", "achieved": p2p_tflops, "peak": peak,
+                "unit": "TFLOP/s", "frac": p2p_tflops / peak}
+    else:
+        a = m2l_flops / (ph["m2l"] * 1e-3) / 1e12
+        roof = {"kernel": "k_m2l + k_l2l (M2L, O(P^4))", "bound": "alu", "achieved": a, "peak": peak,
+                "unit": "TFLOP/s", "frac": a / peak}
+    roof["traffic"] = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            tr = json.load(open(prof))
+            if tr.get("config") == wname and roof["kernel"].split()[0] in tr:
+                roof["traffic"] = tr[roof["kernel"].split()[0]]
+        except Exception:
+            pass
+
+    out = {"metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
+           "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": wname, "n_panels": n, "n_charges": len(cfg["charge_q"]), "terms": P,
+                      "quad_points": 1, "leaf_points": args.leaf_points, "operator": "A = I - f K'",
+                      "tree_levels": info["levels"], "n_leaves": info["n_leaves"],
+                      "l2_flush": "inputs larger than L2 (x 409 MB, points 3.3 GB)",
+                      "parallelism": "single GPU" if world == 1 else f"replicas x{world}"},
+           "matvec_s": ms * 1e-3,
+           "phases_ms": ph,
+           "p2p_ginteractions_s": p2p_int / p2p_s / 1e9,
+           "p2p_interactions": p2p_int,
+           "p2p_frac_fp32_peak": p2p_tflops / peak,
+           "m2l_pairs": m2l_pairs,
+           "setup_s": setup_s,
+           "bibee_cfa": {"dG_kcal_mol": bib["dG_kcal"], "first_call_s": bibee_s, "warm_s": bibee_warm_s},
+           "roofline": roof,
+           "gpu_launches": args.steps * (4 + 2 * max(0, info["levels"] - 2)),
+           "e2e": {"value": 1.0 / e2e_s, "unit": "matvec/s", "h2d_bytes_per_step": 4 * n,
+                   "d2h_bytes_per_step": 4 * n},
+           "clocks": clocks}
+    if rank == 0 and not args.no_cpu:
+        rows = np.random.default_rng(11).choice(n, args.cpu_rows, replace=False)
+        y_ref, dt, cores, _ = oracle_sample(cfg, rows, x_global)
+        y_loc = y.cpu().numpy().astype(np.float64)
+        y_glob = s.to_global(y_loc)
+        f = 2.0 * (80.0 - 4.0) / 84.0
+        a_ref = x_global[rows] - f * y_ref
+        out["parity_sampled_rows"] = {"rows": int(len(rows)),
+                                      "rel_l2_A": float(np.linalg.norm(y_glob[rows] - a_ref) / np.linalg.norm(a_ref)),
+                                      "rel_l2_Kprime": float(np.linalg.norm((x_global[rows] - y_glob[rows]) / f - y_ref)
+                                                             / np.linalg.norm(y_ref))}
+        t_full = dt / len(rows) * n
+        out["cpu_baseline"] = {"value": 1.0 / t_full, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+                               "sample": f"{len(rows)} target rows x {n} sources (FP64 direct K' rows, "
+                                         f"{dt:.1f} s), extrapolated to the full {n}-row matvec"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,184 @@
+/* fmmbem.h -- C ABI of the B200-native FMM-BEM hot path (arXiv 1007.4591).
+ *
+ * Pure C: no CUDA, NCCL or PyTorch types appear here.  Device pointers are plain
+ * `float*`/`double*` in CUDA device memory of the ctx's device; streams are passed
+ * as `void*` (a cudaStream_t, NULL = the legacy default stream).
+ *
+ * The user's problem (Sec. 2.1): given a closed triangulated
+ * dielectric boundary Omega, interior point charges (q_i, r_i) and eps_I, eps_II,
+ * compute the induced surface charge sigma of the second-kind integral equation
+ * (Eq. 4) and the solvation energy dG = 1/2 sum q_i phi_reac(r_i)
+ * (Eq. 5-6), either exactly (GMRES on A x = B q) or by the
+ * BIBEE diagonal approximation (Eq. 7).  Discretisation: flat panels,
+ * piecewise-constant sigma, K-point quadrature (K = 1 = the paper's centroid rule,
+ * P:409-411).  Readings of the paper are listed in DESIGN.md (A1-A22).
+ *
+ * Ownership: fmmbem_create deep-copies every host input (the caller may free them on
+ * return).  The ctx owns all of its device memory.  All output buffers are caller-owned.
+ * Errors: every call returns fmmbem_status; nothing throws across the ABI; on a
+ * negative status no output has been written ("no partial outputs") and
+ * fmmbem_last_error() names the offending index.  A ctx is not thread-safe.
+ * Units: Angstrom and elementary charges; energies in internal units (kernels with the
+ * explicit 1/(4 pi) of Eq. 4-5) and in kcal/mol = internal * 4 pi * 332.0637.
+ */
+#ifndef FMMBEM_H
+#define FMMBEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMMBEM_ABI_VERSION 1
+
+typedef struct fmmbem_ctx fmmbem_ctx; /* opaque */
+
+typedef enum {
+  FMMBEM_OK = 0,
+  FMMBEM_NOT_CONVERGED = 1,  /* solve: outputs hold the best iterate */
+  FMMBEM_E_INVALID = -1,     /* null/size/NaN input, eps <= 0, eps_in == eps_out, bad options */
+  FMMBEM_E_DEGENERATE = -2,  /* triangle index out of range or area < 1e-14*bbox_diag^2 */
+  FMMBEM_E_COINCIDENT = -3,  /* charge on a panel point, duplicate centroids */
+  FMMBEM_E_CUDA = -4,
+  FMMBEM_E_NOMEM = -5,
+  FMMBEM_E_NCCL = -6
+} fmmbem_status;
+
+/* Surface mesh: n_vertices x 3 doubles (Angstrom), n_triangles x 3 int32 vertex indices,
+ * 0-based, outward winding (normal = cross(v1-v0, v2-v0) points into region II). */
+typedef struct {
+  int64_t n_vertices;
+  const double* xyz;
+  int64_t n_triangles;
+  const int32_t* tri;
+} fmmbem_mesh;
+
+/* Point charges: n x 3 positions (Angstrom) and n charges (e); n may be 0. */
+typedef struct {
+  int64_t n;
+  const double* xyz;
+  const double* q;
+} fmmbem_charges;
+
+typedef struct {
+  int32_t struct_size;   /* = sizeof(fmmbem_options) */
+  int32_t terms;         /* P = number of expansion terms, degrees 0..P-1 (A9); 2..16, default 10 */
+  int32_t leaf_points;   /* depth rule: mean panels per occupied leaf <= leaf_points (A10); default 64 */
+  int32_t quad_points;   /* K in {1 (paper), 3, 6, 7}; default 1 */
+  int32_t near_mode;     /* 0 only (analytic near field is a later row); default 0 */
+  float near_radius;     /* reserved */
+  int32_t self_term;     /* 0 only: K'_ii = 0 (flat panel) */
+  int32_t direct;        /* 1 = bypass the FMM: all-pairs P2P (paper Fig. 11 "direct") */
+  int32_t deterministic; /* reductions have a fixed order (no atomics on results); always true */
+  int32_t device;        /* CUDA ordinal used by this ctx */
+  int32_t rank, nranks;  /* one process per GPU; nranks > 1 is reserved (returns E_INVALID) */
+  const void* nccl_id;   /* reserved for nranks > 1 */
+} fmmbem_options;
+
+/* Fill *out with the defaults above.  Returns FMMBEM_E_INVALID if out is NULL. */
+fmmbem_status fmmbem_default_options(fmmbem_options* out);
+
+/* Build the solver for one molecule (setup): validates and
+ * deep-copies the inputs, derives panels and quadrature points (FP64, P:368-378,
+ * P:409-411), builds the Morton-sorted uniform-depth octree, its neighbour and
+ * interaction lists on the device.  opt may be NULL (defaults).
+ * On success *out receives a new ctx; on failure *out is set to NULL. */
+fmmbem_status fmmbem_create(const fmmbem_mesh* panels, const fmmbem_charges* charges,
+                            double eps_in, double eps_out, const fmmbem_options* opt,
+                            fmmbem_ctx** out);
+
+/* Release every resource of ctx.  NULL-safe. */
+void fmmbem_destroy(fmmbem_ctx* ctx);
+
+/* Vectors passed to matvec/solve/bibee are in the library's LOCAL order (the octree's
+ * Morton order).  fmmbem_local_panel_ids writes, for local index i, the caller's
+ * triangle index (host int64 array of fmmbem_num_local_panels entries). */
+int64_t fmmbem_num_local_panels(const fmmbem_ctx* ctx);
+fmmbem_status fmmbem_local_panel_ids(const fmmbem_ctx* ctx, int64_t* global_ids_out);
+
+typedef enum {
+  FMMBEM_OP_KPRIME = 0, /* y_i = sum_{j!=i} A_j x_j sum_g w_g dG/dn_i(c_i, y_jg)   (Eq. 4 operator) */
+  FMMBEM_OP_SINGLE = 1, /* y_i = sum_{j!=i} A_j x_j sum_g w_g G(c_i, y_jg)         (Eq. 5, 1/r)     */
+  FMMBEM_OP_A = 2       /* y = x - f * KPRIME(x), f = 2(eps_II-eps_I)/(eps_I+eps_II) (GMRES operator, A1) */
+} fmmbem_op;
+
+/* One FMM matrix-vector product.  x_dev, y_dev: caller-owned device
+ * arrays of fmmbem_num_local_panels floats in local order; must not alias.  Stream-ordered:
+ * returns after enqueueing on cuda_stream; y is valid when the stream completes. */
+fmmbem_status fmmbem_matvec(fmmbem_ctx* ctx, fmmbem_op op, const float* x_dev, float* y_dev,
+                            void* cuda_stream);
+
+/* Same product with HOST buffers (pinned or pageable): copies x in, runs, copies y out,
+ * synchronises.  Used for end-to-end timing. */
+fmmbem_status fmmbem_matvec_host(fmmbem_ctx* ctx, fmmbem_op op, const float* x_host, float* y_host);
+
+typedef struct {
+  double tol;           /* relative residual ||b - A x|| / ||b||, default 1e-6 (A12) */
+  int32_t restart;      /* GMRES(m) restart length, default 30 */
+  int32_t max_iters;    /* default 200 */
+  const float* x0_dev;  /* initial guess (device, local order) or NULL = zero */
+} fmmbem_solve_options;
+
+typedef struct {
+  double dG_internal;   /* 1/2 sum_j A_j sigma_j psi_j (= 1/2 q^T C sigma, A20) */
+  double dG_kcal_mol;   /* dG_internal * 4 pi * 332.0637 (A13) */
+  int32_t iterations;   /* GMRES iterations (0 for BIBEE) */
+  double rel_residual;  /* final GMRES relative residual estimate (0 for BIBEE) */
+} fmmbem_energy;
+
+/* Full BEM solve: E_n and psi by one charge-FMM, then GMRES on
+ * (I - f K') sigma = f E_n, then dG.  sigma_dev (nullable): n_local floats; residual_hist
+ * (nullable, host): max_iters+1 doubles, unused entries set to -1.  Returns FMMBEM_OK or
+ * FMMBEM_NOT_CONVERGED (best iterate written). */
+fmmbem_status fmmbem_solve(fmmbem_ctx* ctx, const fmmbem_solve_options* opt, float* sigma_dev,
+                           double* residual_hist, fmmbem_energy* out);
+
+typedef enum {
+  FMMBEM_BIBEE_CFA = 0, /* s = -1/2 (Eq. 7) */
+  FMMBEM_BIBEE_P = 1,   /* s = 0 */
+  FMMBEM_BIBEE_LB = 2   /* s = +1/2 */
+} fmmbem_bibee;
+
+/* BIBEE energy: sigma_hat = f E_n / (1 - f s), dG = 1/2 sum A sigma_hat psi.
+ * sigma_hat_dev nullable (n_local floats). */
+fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* ctx, fmmbem_bibee variant, float* sigma_hat_dev,
+                                  fmmbem_energy* out);
+
+/* Diagnostics: E_n (with 1/eps_I) and psi_j = sum_g w_g sum_k q_k G(y_jg, r_k) at the panels
+ * (device, local order; either may be NULL). */
+fmmbem_status fmmbem_charge_fields(fmmbem_ctx* ctx, float* En_dev, float* psi_dev);
+
+/* Reaction potential phi_reac(r_k) = sum_j sigma_j A_j sum_g w_g G(r_k, y_jg) at every charge
+ * (Eq. 5), written to a host array of n_charges doubles in the caller's charge order. */
+fmmbem_status fmmbem_reaction_potential(fmmbem_ctx* ctx, const float* sigma_dev, double* phi_host);
+
+typedef struct {
+  double tree, upward, m2l, p2p, l2p, near, comm, gmres, total; /* ms, last call */
+  int64_t p2p_interactions; /* exact pair count of the last matvec's P2P */
+  int64_t m2l_pairs;        /* M2L translations of the last matvec */
+} fmmbem_timing;
+
+fmmbem_status fmmbem_last_timing(const fmmbem_ctx* ctx, fmmbem_timing* out);
+
+/* Tree statistics for tests / reporting. */
+typedef struct {
+  int32_t levels;       /* leaf level L (root = 0) */
+  int64_t n_leaves;
+  int64_t n_cells;      /* all levels */
+  int64_t n_panels, n_charges;
+  int64_t nbr_pairs;    /* leaf neighbour-list entries (incl. self) */
+  int64_t m2l_pairs;    /* interaction-list entries over all levels */
+  double root_width;    /* root cube width (Angstrom) */
+  double root_origin[3];
+} fmmbem_tree_info;
+
+fmmbem_status fmmbem_tree_info_get(const fmmbem_ctx* ctx, fmmbem_tree_info* out);
+
+/* Thread-local message describing the last error (never NULL). */
+const char* fmmbem_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMMBEM_H */

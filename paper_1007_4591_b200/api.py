@@ -1,0 +1,165 @@
+"""Thin Python wrapper of the C ABI (include/fmmbem.h): argument marshalling only.
+
+Every step of the hot path runs in libfmmbem.so's CUDA kernels; PyTorch is used for
+device tensors and streams.  Vectors are in the library's LOCAL (Morton) order; use
+`local_ids` / `to_local` / `to_global` to map from / to the caller's triangle order.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+
+BIBEE = {"cfa": L.BIBEE_CFA, "p": L.BIBEE_P, "lb": L.BIBEE_LB}
+OPS = {"kprime": L.OP_KPRIME, "single": L.OP_SINGLE, "A": L.OP_A}
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def default_options(**kw):
+    lib = L.load()
+    o = L.Options()
+    L.check(lib.fmmbem_default_options(C.byref(o)))
+    for k, v in kw.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown option {k}")
+        setattr(o, k, v)
+    return o
+
+
+class Solver:
+    """One molecule: fmmbem_create(...) + the calls of the C ABI."""
+
+    def __init__(self, vertices, triangles, charge_xyz=None, charge_q=None, eps_in=4.0, eps_out=80.0,
+                 **options):
+        import torch
+        self._torch = torch
+        self.lib = L.load()
+        v = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+        cx = np.ascontiguousarray(np.zeros((0, 3)) if charge_xyz is None else charge_xyz, np.float64).reshape(-1, 3)
+        cq = np.ascontiguousarray(np.zeros(0) if charge_q is None else charge_q, np.float64).reshape(-1)
+        if len(cx) != len(cq):
+            raise ValueError("charge_xyz and charge_q differ in length")
+        self.options = default_options(**options)
+        self.device = int(self.options.device)
+        mesh = L.Mesh(len(v), _dp(v), len(t), t.ctypes.data_as(C.POINTER(C.c_int32)))
+        chg = L.Charges(len(cq), _dp(cx) if len(cq) else None, _dp(cq) if len(cq) else None)
+        h = C.c_void_p()
+        L.check(self.lib.fmmbem_create(C.byref(mesh), C.byref(chg), float(eps_in), float(eps_out),
+                                       C.byref(self.options), C.byref(h)))
+        self._h = h
+        self.n = int(self.lib.fmmbem_num_local_panels(h))
+        ids = np.empty(self.n, np.int64)
+        L.check(self.lib.fmmbem_local_panel_ids(h, ids.ctypes.data_as(C.POINTER(C.c_int64))))
+        self.local_ids = ids
+        self.n_charges = len(cq)
+        self.eps_in, self.eps_out = float(eps_in), float(eps_out)
+
+    @classmethod
+    def from_config(cls, cfg, **options):
+        return cls(cfg["vertices"], cfg["triangles"], cfg["charge_xyz"], cfg["charge_q"], cfg["eps_in"],
+                   cfg["eps_out"], **options)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.fmmbem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- order helpers
+    def to_local(self, x_global):
+        return np.asarray(x_global)[self.local_ids]
+
+    def to_global(self, x_local):
+        x_local = np.asarray(x_local)
+        out = np.empty_like(x_local)
+        out[self.local_ids] = x_local
+        return out
+
+    def _dev(self):
+        return self._torch.device("cuda", self.device)
+
+    def _vec(self, x):
+        torch = self._torch
+        if not isinstance(x, torch.Tensor):
+            x = torch.as_tensor(np.asarray(x, np.float32))
+        x = x.to(device=self._dev(), dtype=torch.float32).contiguous()
+        if x.numel() != self.n:
+            raise ValueError(f"vector of {x.numel()} entries, expected {self.n}")
+        return x
+
+    # ---- ABI calls
+    def matvec(self, x, op="kprime", out=None, stream=None):
+        """y = op(x) on the GPU (local order); x: torch CUDA float32 tensor or array."""
+        torch = self._torch
+        x = self._vec(x)
+        y = torch.empty_like(x) if out is None else out
+        st = torch.cuda.current_stream(self._dev()) if stream is None else stream
+        L.check(self.lib.fmmbem_matvec(self._h, OPS[op], C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                       C.c_void_p(st.cuda_stream)))
+        return y
+
+    def matvec_host(self, x_host, op="kprime", y_host=None):
+        """End-to-end product with host buffers (copies inside the library)."""
+        x = np.ascontiguousarray(x_host, np.float32)
+        y = np.empty_like(x) if y_host is None else y_host
+        L.check(self.lib.fmmbem_matvec_host(self._h, OPS[op], C.c_void_p(x.ctypes.data),
+                                            C.c_void_p(y.ctypes.data)))
+        return y
+
+    def charge_fields(self):
+        torch = self._torch
+        En = torch.empty(self.n, device=self._dev(), dtype=torch.float32)
+        psi = torch.empty_like(En)
+        L.check(self.lib.fmmbem_charge_fields(self._h, C.c_void_p(En.data_ptr()), C.c_void_p(psi.data_ptr())))
+        return En, psi
+
+    def bibee(self, variant="cfa", want_sigma=False):
+        torch = self._torch
+        e = L.Energy()
+        sig = torch.empty(self.n, device=self._dev(), dtype=torch.float32) if want_sigma else None
+        L.check(self.lib.fmmbem_bibee_energy(self._h, BIBEE[variant],
+                                             C.c_void_p(sig.data_ptr()) if sig is not None else None, C.byref(e)))
+        out = dict(dG=e.dG_internal, dG_kcal=e.dG_kcal_mol)
+        if sig is not None:
+            out["sigma"] = sig
+        return out
+
+    def solve(self, tol=1e-6, restart=30, max_iters=200, x0=None):
+        torch = self._torch
+        so = L.SolveOptions(tol, restart, max_iters, C.c_void_p(x0.data_ptr()) if x0 is not None else None)
+        sig = torch.empty(self.n, device=self._dev(), dtype=torch.float32)
+        hist = np.empty(max_iters + 1, np.float64)
+        e = L.Energy()
+        code = L.check(self.lib.fmmbem_solve(self._h, C.byref(so), C.c_void_p(sig.data_ptr()),
+                                             hist.ctypes.data_as(C.POINTER(C.c_double)), C.byref(e)))
+        return dict(sigma=sig, dG=e.dG_internal, dG_kcal=e.dG_kcal_mol, iterations=e.iterations,
+                    rel_residual=e.rel_residual, converged=(code == L.OK), history=hist[hist >= 0])
+
+    def reaction_potential(self, sigma):
+        sigma = self._vec(sigma)
+        phi = np.empty(self.n_charges, np.float64)
+        L.check(self.lib.fmmbem_reaction_potential(self._h, C.c_void_p(sigma.data_ptr()), _dp(phi)))
+        return phi
+
+    def timing(self):
+        t = L.Timing()
+        L.check(self.lib.fmmbem_last_timing(self._h, C.byref(t)))
+        return {k: getattr(t, k) for k, _ in L.Timing._fields_}
+
+    def tree_info(self):
+        t = L.TreeInfo()
+        L.check(self.lib.fmmbem_tree_info_get(self._h, C.byref(t)))
+        d = {k: getattr(t, k) for k, _ in L.TreeInfo._fields_}
+        d["root_origin"] = list(t.root_origin)
+        return d

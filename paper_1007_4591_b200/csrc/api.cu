@@ -1,0 +1,573 @@
+// api.cu -- the C ABI of libfmmbem (include/fmmbem.h) and the orchestration of one FMM
+// evaluation.  Every step of the path runs in this library's kernels;
+// the host only validates, launches and runs the small FP64 GMRES least-squares problem.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "kernels.cuh"
+
+static thread_local std::string g_err = "";
+
+namespace fmm {
+
+namespace {
+
+constexpr double FOUR_PI = 12.566370614359172953850573533118;
+constexpr double KCAL = 4.0 * 3.14159265358979323846 * 332.0637;  // SPEC S:409 (A13)
+
+// Appendix C quadrature rules (barycentric beta, weight); K = 1 is the paper's centroid rule
+// (P:409-411).  Independent copy of the table (the oracle keeps its own).
+void quad_rule(int K, std::vector<double>& beta, std::vector<double>& w) {
+  beta.clear();
+  w.clear();
+  auto add3 = [&](double a, double b, double wt) {
+    double p[3][3] = {{a, b, b}, {b, a, b}, {b, b, a}};
+    for (auto& r : p) {
+      beta.insert(beta.end(), r, r + 3);
+      w.push_back(wt);
+    }
+  };
+  if (K == 1) {
+    beta = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+    w = {1.0};
+  } else if (K == 3) {
+    add3(2.0 / 3, 1.0 / 6, 1.0 / 3);
+  } else if (K == 6) {
+    add3(0.108103018168070, 0.445948490915965, 0.223381589678011);
+    add3(0.816847572980459, 0.091576213509771, 0.109951743655322);
+  } else if (K == 7) {
+    beta = {1.0 / 3, 1.0 / 3, 1.0 / 3};
+    w = {0.225};
+    add3(0.059715871789770, 0.470142064105115, 0.132394152788506);
+    add3(0.797426985353087, 0.101286507323456, 0.125939180544827);
+  }
+}
+
+// Panel prep: FP64 centroid, unit normal from
+// the winding, area, quadrature points; flags index-out-of-range and degenerate triangles.
+__global__ void k_prep(int64_t np, int64_t nv, const double* __restrict__ V, const int* __restrict__ T, int K,
+                       const double* __restrict__ beta, double atol, double* cen, double* nrm, double* area,
+                       double* qp, int* bad) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  int a = T[3 * i], b = T[3 * i + 1], c = T[3 * i + 2];
+  if (a < 0 || b < 0 || c < 0 || a >= nv || b >= nv || c >= nv) {
+    atomicMin(bad, (int)i);
+    return;
+  }
+  const double* A = V + 3 * (int64_t)a;
+  const double* B = V + 3 * (int64_t)b;
+  const double* C = V + 3 * (int64_t)c;
+  double e1[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+  double e2[3] = {C[0] - A[0], C[1] - A[1], C[2] - A[2]};
+  double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+  double nn = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+  if (!(0.5 * nn >= atol)) {
+    atomicMin(bad, (int)i);
+    return;
+  }
+  for (int d = 0; d < 3; ++d) {
+    cen[3 * i + d] = (A[d] + B[d] + C[d]) / 3.0;
+    nrm[3 * i + d] = cr[d] / nn;
+  }
+  area[i] = 0.5 * nn;
+  if (qp)
+    for (int g = 0; g < K; ++g)
+      for (int d = 0; d < 3; ++d)
+        qp[(i * K + g) * 3 + d] = beta[3 * g] * A[d] + beta[3 * g + 1] * B[d] + beta[3 * g + 2] * C[d];
+}
+
+__global__ void k_scale(float* y, const float* x, int64_t n, float s) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = s * x[i];
+}
+
+// psi_j = sum_g (A_j w_g / A_j) psi_jg
+__global__ void k_quad_reduce(int64_t np, int K, const float* __restrict__ psiq, const float4* __restrict__ qpos,
+                              const float4* __restrict__ ppos, float* psi) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  float s = 0.f, ia = 1.f / ppos[i].w;
+  for (int g = 0; g < K; ++g) s = fmaf(qpos[i * K + g].w * ia, psiq[i * K + g], s);
+  psi[i] = s;
+}
+
+__global__ void k_unpermute(int64_t n, const int* __restrict__ ids, const float* __restrict__ v, double* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[ids[i]] = (double)v[i];
+}
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+const SrcArg kp_src(fmmbem_ctx* c, const float* x) {
+  SrcArg s;
+  s.set = (c->K == 1) ? &c->pan : &c->quad;
+  s.x = x;
+  return s;
+}
+
+}  // namespace
+
+void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
+              cudaStream_t st, bool timing) {
+  const bool direct = c->opt.direct != 0 || c->tree.L < 2;
+  if (timing) cudaEventRecord(c->ev[0], st);
+  if (!direct) {
+    launch_upward(c, s, st);
+    if (timing) cudaEventRecord(c->ev[1], st);
+    launch_m2l(c, *s.set, *t.set, st);
+    launch_downward(c, *t.set, st);
+    if (timing) cudaEventRecord(c->ev[2], st);
+  } else if (timing) {
+    cudaEventRecord(c->ev[1], st);
+    cudaEventRecord(c->ev[2], st);
+  }
+  launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
+  if (timing) cudaEventRecord(c->ev[3], st);
+  if (!direct) {
+    Outputs acc = o;
+    acc.pot.x = nullptr;
+    acc.dn.x = nullptr;
+    launch_l2p(c, t, acc, st);
+  }
+  if (timing) cudaEventRecord(c->ev[4], st);
+}
+
+void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_t st, bool timing) {
+  TgtArg t;
+  t.set = &c->pan;
+  Outputs o;
+  if (op == FMMBEM_OP_SINGLE) {
+    o.pot.y = y;
+    o.pot.b = (float)(1.0 / FOUR_PI);
+  } else {
+    o.dn.y = y;
+    if (op == FMMBEM_OP_KPRIME) {
+      o.dn.b = (float)(1.0 / FOUR_PI);
+    } else {  // A = I - f K'
+      o.dn.x = x;
+      o.dn.ax = 1.f;
+      o.dn.b = (float)(-c->f / FOUR_PI);
+    }
+  }
+  fmm_eval(c, t, kp_src(c, x), o, /*self=*/true, /*check=*/false, st, timing);
+}
+
+void apply_A(fmmbem_ctx* c, const float* x, float* y, cudaStream_t s) { apply_op(c, FMMBEM_OP_A, x, y, s, false); }
+
+void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
+  if (c->have_fields) return;
+  c->En.alloc(c->np);
+  c->psi.alloc(c->np);
+  if (c->nc == 0) {
+    c->En.zero(st);
+    c->psi.zero(st);
+    c->have_fields = true;
+    return;
+  }
+  FMM_CUDA(cudaMemsetAsync(c->flag.get(), 0, sizeof(int), st));
+  TgtArg t;
+  t.set = &c->pan;
+  SrcArg s;
+  s.set = &c->chg;
+  Outputs o;
+  o.dn.y = c->En.get();
+  o.dn.b = (float)(1.0 / (FOUR_PI * c->eps_in));  // E_n carries 1/eps_I (Eq. 1, reading A2)
+  if (c->K == 1) {
+    o.pot.y = c->psi.get();
+    o.pot.b = (float)(1.0 / FOUR_PI);
+  }
+  fmm_eval(c, t, s, o, false, true, st, false);
+  if (c->K > 1) {
+    DevBuf<float> psiq;
+    psiq.alloc(c->quad.n);
+    TgtArg tq;
+    tq.set = &c->quad;
+    Outputs oq;
+    oq.pot.y = psiq.get();
+    oq.pot.b = (float)(1.0 / FOUR_PI);
+    fmm_eval(c, tq, s, oq, false, true, st, false);
+    k_quad_reduce<<<ceil_div(c->np, 256), 256, 0, st>>>(c->np, c->K, psiq.get(), c->quad.pos.get(), c->pan.pos.get(),
+                                                        c->psi.get());
+    FMM_CHECK_LAUNCH();
+    FMM_CUDA(cudaStreamSynchronize(st));
+  }
+  int flag = 0;
+  FMM_CUDA(cudaMemcpyAsync(&flag, c->flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  if (flag) throw Error(FMMBEM_E_COINCIDENT, "a charge coincides with a panel quadrature point");
+  c->have_fields = true;
+}
+
+void fill_timing(fmmbem_ctx* c, bool direct) {
+  float t[5] = {0, 0, 0, 0, 0};
+  cudaEventSynchronize(c->ev[4]);
+  for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], c->ev[i], c->ev[i + 1]);
+  fmmbem_timing& T = c->last;
+  const double g = T.gmres;
+  std::memset(&T, 0, sizeof(T));
+  T.gmres = g;
+  T.upward = t[0];
+  T.m2l = t[1];
+  T.p2p = t[2];
+  T.l2p = t[3];
+  T.total = t[0] + t[1] + t[2] + t[3];
+  T.p2p_interactions = c->p2p_inter_kp;
+  T.m2l_pairs = direct ? 0 : c->m2l_pairs_kp;
+}
+
+}  // namespace fmm
+
+using namespace fmm;
+
+#define API_BEGIN try {
+#define API_END                                    \
+  }                                                \
+  catch (const fmm::Error& e) {                    \
+    g_err = e.what();                              \
+    return e.code;                                 \
+  }                                                \
+  catch (const std::exception& e) {                \
+    g_err = e.what();                              \
+    return FMMBEM_E_CUDA;                          \
+  }
+
+extern "C" {
+
+const char* fmmbem_last_error(void) { return g_err.c_str(); }
+
+fmmbem_status fmmbem_default_options(fmmbem_options* o) {
+  if (!o) return FMMBEM_E_INVALID;
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(fmmbem_options);
+  o->terms = 10;
+  o->leaf_points = 64;
+  o->quad_points = 1;
+  o->near_mode = 0;
+  o->near_radius = 3.f;
+  o->self_term = 0;
+  o->direct = 0;
+  o->deterministic = 1;
+  o->device = 0;
+  o->rank = 0;
+  o->nranks = 1;
+  o->nccl_id = nullptr;
+  return FMMBEM_OK;
+}
+
+fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, double eps_in, double eps_out,
+                            const fmmbem_options* opt_in, fmmbem_ctx** out) {
+  if (out) *out = nullptr;
+  fmmbem_ctx* c = nullptr;
+  API_BEGIN
+  if (!out || !mesh) throw Error(FMMBEM_E_INVALID, "null argument");
+  fmmbem_options opt;
+  fmmbem_default_options(&opt);
+  if (opt_in) {
+    if (opt_in->struct_size != (int)sizeof(fmmbem_options)) throw Error(FMMBEM_E_INVALID, "options.struct_size mismatch");
+    opt = *opt_in;
+  }
+  if (opt.terms < 2 || opt.terms > MAX_TERMS) throw Error(FMMBEM_E_INVALID, "terms must be in [2, 16]");
+  if (opt.leaf_points < 1) throw Error(FMMBEM_E_INVALID, "leaf_points must be >= 1");
+  if (!(opt.quad_points == 1 || opt.quad_points == 3 || opt.quad_points == 6 || opt.quad_points == 7))
+    throw Error(FMMBEM_E_INVALID, "quad_points must be 1, 3, 6 or 7");
+  if (opt.near_mode != 0) throw Error(FMMBEM_E_INVALID, "near_mode = 1 (analytic near field) is not available yet");
+  if (opt.self_term != 0) throw Error(FMMBEM_E_INVALID, "self_term = 1 is not available yet");
+  if (opt.nranks != 1 || opt.rank != 0) throw Error(FMMBEM_E_INVALID, "nranks > 1 is not available yet");
+  if (!(eps_in > 0) || !(eps_out > 0) || eps_in == eps_out || !std::isfinite(eps_in) || !std::isfinite(eps_out))
+    throw Error(FMMBEM_E_INVALID, "need eps_in, eps_out > 0 and eps_in != eps_out");
+  if (mesh->n_triangles < 1 || mesh->n_vertices < 3 || !mesh->xyz || !mesh->tri)
+    throw Error(FMMBEM_E_INVALID, "empty mesh");
+  const int64_t nc = chg ? chg->n : 0;
+  if (nc < 0 || (nc > 0 && (!chg->xyz || !chg->q))) throw Error(FMMBEM_E_INVALID, "bad charges");
+  if (mesh->n_triangles * (int64_t)opt.quad_points >= (1LL << 31) || mesh->n_vertices >= (1LL << 31))
+    throw Error(FMMBEM_E_INVALID, "problem too large for 32-bit point indices");
+  for (int64_t i = 0; i < 3 * mesh->n_vertices; ++i)
+    if (!std::isfinite(mesh->xyz[i])) throw Error(FMMBEM_E_INVALID, "non-finite vertex " + std::to_string(i / 3));
+  for (int64_t i = 0; i < nc; ++i) {
+    if (!std::isfinite(chg->q[i]) || !std::isfinite(chg->xyz[3 * i]) || !std::isfinite(chg->xyz[3 * i + 1]) ||
+        !std::isfinite(chg->xyz[3 * i + 2]))
+      throw Error(FMMBEM_E_INVALID, "non-finite charge " + std::to_string(i));
+  }
+  c = new fmmbem_ctx();
+  c->opt = opt;
+  c->device = opt.device;
+  DevGuard dg(c->device);
+  FMM_CUDA(cudaSetDevice(c->device));
+  FMM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
+  c->P = opt.terms;
+  c->NC = c->P * (c->P + 1) / 2;
+  c->K = opt.quad_points;
+  c->eps_in = eps_in;
+  c->eps_out = eps_out;
+  c->f = 2.0 * (eps_out - eps_in) / (eps_in + eps_out);  // reading A1
+  c->eps_hat = 1.0 - eps_in / eps_out;
+  c->np = mesh->n_triangles;
+  c->nc = nc;
+  cudaStream_t s = c->stream;
+  const int64_t np = c->np, nv = mesh->n_vertices;
+  // upload + panel prep
+  DevBuf<double> dV, cen, nrm, area, qp, beta, wq, cx, cq;
+  DevBuf<int> dT;
+  dV.alloc(3 * nv);
+  dT.alloc(3 * np);
+  FMM_CUDA(cudaMemcpyAsync(dV.get(), mesh->xyz, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaMemcpyAsync(dT.get(), mesh->tri, 3 * np * sizeof(int), cudaMemcpyHostToDevice, s));
+  std::vector<double> hb, hw;
+  quad_rule(c->K, hb, hw);
+  beta.alloc(hb.size());
+  wq.alloc(hw.size());
+  FMM_CUDA(cudaMemcpyAsync(beta.get(), hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaMemcpyAsync(wq.get(), hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = 0; i < nv; ++i)
+    for (int d = 0; d < 3; ++d) {
+      mn[d] = std::min(mn[d], mesh->xyz[3 * i + d]);
+      mx[d] = std::max(mx[d], mesh->xyz[3 * i + d]);
+    }
+  double diag2 = 0;
+  for (int d = 0; d < 3; ++d) diag2 += (mx[d] - mn[d]) * (mx[d] - mn[d]);
+  cen.alloc(3 * np);
+  nrm.alloc(3 * np);
+  area.alloc(np);
+  if (c->K > 1) qp.alloc(3 * np * c->K);
+  c->flag.alloc(4);
+  int big = 0x7fffffff;
+  FMM_CUDA(cudaMemcpyAsync(c->flag.get(), &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  k_prep<<<ceil_div(np, 256), 256, 0, s>>>(np, nv, dV.get(), dT.get(), c->K, beta.get(), 1e-14 * diag2, cen.get(),
+                                           nrm.get(), area.get(), c->K > 1 ? qp.get() : nullptr, c->flag.get());
+  FMM_CHECK_LAUNCH();
+  int bad = 0;
+  FMM_CUDA(cudaMemcpyAsync(&bad, c->flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  if (bad != big) {
+    const int* t = mesh->tri + 3 * (int64_t)bad;
+    bool range = t[0] < 0 || t[1] < 0 || t[2] < 0 || t[0] >= nv || t[1] >= nv || t[2] >= nv;
+    throw Error(FMMBEM_E_DEGENERATE, std::string(range ? "triangle index out of range" : "degenerate triangle") +
+                                         " " + std::to_string(bad));
+  }
+  dV.release();
+  dT.release();
+  if (nc) {
+    cx.alloc(3 * nc);
+    cq.alloc(nc);
+    FMM_CUDA(cudaMemcpyAsync(cx.get(), chg->xyz, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, s));
+    FMM_CUDA(cudaMemcpyAsync(cq.get(), chg->q, nc * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  build_tree(c, cen.get(), nrm.get(), area.get(), qp.get(), wq.get(), cx.get(), cq.get(), s);
+  init_tables(c);
+  c->Mx.alloc((size_t)c->tree.n_cells * c->NC);
+  c->Lx.alloc((size_t)c->tree.n_cells * c->NC);
+  c->red.alloc(64);
+  const PointSet& src = (c->K == 1) ? c->pan : c->quad;
+  c->p2p_inter_kp = count_p2p(c, c->pan, src, true, c->opt.direct != 0 || c->tree.L < 2);
+  c->m2l_pairs_kp = (c->opt.direct != 0 || c->tree.L < 2) ? 0 : c->tree.m2l_pairs;
+  FMM_CUDA(cudaStreamSynchronize(s));
+  *out = c;
+  return FMMBEM_OK;
+  }
+  catch (const fmm::Error& e) {
+    g_err = e.what();
+    fmmbem_destroy(c);
+    return e.code;
+  }
+  catch (const std::exception& e) {
+    g_err = e.what();
+    fmmbem_destroy(c);
+    return FMMBEM_E_CUDA;
+  }
+}
+
+void fmmbem_destroy(fmmbem_ctx* c) {
+  if (!c) return;
+  {
+    DevGuard dg(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+  }
+}
+
+int64_t fmmbem_num_local_panels(const fmmbem_ctx* c) { return c ? c->np : 0; }
+
+fmmbem_status fmmbem_local_panel_ids(const fmmbem_ctx* c, int64_t* ids) {
+  if (!c || !ids) return FMMBEM_E_INVALID;
+  std::memcpy(ids, c->pan_ids.data(), c->np * sizeof(int64_t));
+  return FMMBEM_OK;
+}
+
+fmmbem_status fmmbem_matvec(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, void* stream) {
+  API_BEGIN
+  if (!c || !x || !y || x == y) throw Error(FMMBEM_E_INVALID, "matvec: null or aliased vectors");
+  if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_A) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
+  DevGuard dg(c->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  apply_op(c, op, x, y, st, true);
+  return FMMBEM_OK;
+  API_END
+}
+
+fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* yh) {
+  API_BEGIN
+  if (!c || !xh || !yh) throw Error(FMMBEM_E_INVALID, "matvec_host: null vectors");
+  DevGuard dg(c->device);
+  cudaStream_t st = c->stream;
+  c->tmp_x.alloc(c->np);
+  c->tmp_y.alloc(c->np);
+  FMM_CUDA(cudaMemcpyAsync(c->tmp_x.get(), xh, c->np * sizeof(float), cudaMemcpyHostToDevice, st));
+  apply_op(c, op, c->tmp_x.get(), c->tmp_y.get(), st, true);
+  FMM_CUDA(cudaMemcpyAsync(yh, c->tmp_y.get(), c->np * sizeof(float), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  return FMMBEM_OK;
+  API_END
+}
+
+fmmbem_status fmmbem_charge_fields(fmmbem_ctx* c, float* En, float* psi) {
+  API_BEGIN
+  if (!c) throw Error(FMMBEM_E_INVALID, "null ctx");
+  DevGuard dg(c->device);
+  ensure_fields(c, c->stream);
+  if (En) FMM_CUDA(cudaMemcpyAsync(En, c->En.get(), c->np * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  if (psi) FMM_CUDA(cudaMemcpyAsync(psi, c->psi.get(), c->np * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  FMM_CUDA(cudaStreamSynchronize(c->stream));
+  return FMMBEM_OK;
+  API_END
+}
+
+fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* c, fmmbem_bibee v, float* sig, fmmbem_energy* out) {
+  API_BEGIN
+  if (!c || !out) throw Error(FMMBEM_E_INVALID, "null argument");
+  if (v < FMMBEM_BIBEE_CFA || v > FMMBEM_BIBEE_LB) throw Error(FMMBEM_E_INVALID, "bad BIBEE variant");
+  DevGuard dg(c->device);
+  cudaStream_t st = c->stream;
+  ensure_fields(c, st);
+  const double s = (v == FMMBEM_BIBEE_CFA) ? -0.5 : (v == FMMBEM_BIBEE_P ? 0.0 : 0.5);
+  const double d = 1.0 - c->f * s;
+  if (d == 0.0) throw Error(FMMBEM_E_INVALID, "1 - f s == 0 (SPEC S:383)");
+  DevBuf<float> tmp;
+  float* sh = sig;
+  if (!sh) {
+    tmp.alloc(c->np);
+    sh = tmp.get();
+  }
+  // sigma_hat = f E / (1 - f s)   (Eq. 7 with K' -> s I, reading A3)
+  k_scale<<<ceil_div(c->np, 256), 256, 0, st>>>(sh, c->En.get(), c->np, (float)(c->f / d));
+  FMM_CHECK_LAUNCH();
+  const double e = 0.5 * dot_weighted(c, c->np, sh, c->psi.get(), c->pan.pos.get(), st);  // A20
+  out->dG_internal = e;
+  out->dG_kcal_mol = e * KCAL;
+  out->iterations = 0;
+  out->rel_residual = 0.0;
+  return FMMBEM_OK;
+  API_END
+}
+
+fmmbem_status fmmbem_solve(fmmbem_ctx* c, const fmmbem_solve_options* so, float* sigma, double* hist,
+                           fmmbem_energy* out) {
+  API_BEGIN
+  if (!c || !out) throw Error(FMMBEM_E_INVALID, "null argument");
+  fmmbem_solve_options o{1e-6, 30, 200, nullptr};
+  if (so) o = *so;
+  if (!(o.tol > 0 && o.tol < 1) || o.restart < 1 || o.max_iters < 1)
+    throw Error(FMMBEM_E_INVALID, "bad solve options");
+  DevGuard dg(c->device);
+  cudaStream_t st = c->stream;
+  ensure_fields(c, st);
+  if (c->red.n < (size_t)o.restart + 2) c->red.alloc(o.restart + 2 + 64);
+  DevBuf<float> b, xs;
+  b.alloc(c->np);
+  float* x = sigma;
+  if (!x) {
+    xs.alloc(c->np);
+    x = xs.get();
+  }
+  k_scale<<<ceil_div(c->np, 256), 256, 0, st>>>(b.get(), c->En.get(), c->np, (float)c->f);  // b = f E
+  FMM_CHECK_LAUNCH();
+  if (hist)
+    for (int i = 0; i <= o.max_iters; ++i) hist[i] = -1.0;
+  int its = 0;
+  double rr = 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  fmmbem_status stt = gmres_solve(c, b.get(), x, o.tol, o.restart, o.max_iters, o.x0_dev, hist, &its, &rr, st);
+  cudaEventRecord(e1, st);
+  const double e = 0.5 * dot_weighted(c, c->np, x, c->psi.get(), c->pan.pos.get(), st);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  c->last.gmres = ms;
+  out->dG_internal = e;
+  out->dG_kcal_mol = e * KCAL;
+  out->iterations = its;
+  out->rel_residual = rr;
+  return stt;
+  API_END
+}
+
+fmmbem_status fmmbem_reaction_potential(fmmbem_ctx* c, const float* sigma, double* phi) {
+  API_BEGIN
+  if (!c || !sigma || !phi) throw Error(FMMBEM_E_INVALID, "null argument");
+  if (c->nc == 0) return FMMBEM_OK;
+  DevGuard dg(c->device);
+  cudaStream_t st = c->stream;
+  DevBuf<float> y;
+  DevBuf<double> yd;
+  y.alloc(c->nc);
+  yd.alloc(c->nc);
+  TgtArg t;
+  t.set = &c->chg;
+  Outputs o;
+  o.pot.y = y.get();
+  o.pot.b = (float)(1.0 / FOUR_PI);
+  fmm_eval(c, t, kp_src(c, sigma), o, false, false, st, false);
+  k_unpermute<<<ceil_div(c->nc, 256), 256, 0, st>>>(c->nc, c->chg_ids.get(), y.get(), yd.get());
+  FMM_CHECK_LAUNCH();
+  FMM_CUDA(cudaMemcpyAsync(phi, yd.get(), c->nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  return FMMBEM_OK;
+  API_END
+}
+
+fmmbem_status fmmbem_last_timing(const fmmbem_ctx* c, fmmbem_timing* out) {
+  API_BEGIN
+  if (!c || !out) throw Error(FMMBEM_E_INVALID, "null argument");
+  DevGuard dg(c->device);
+  fill_timing(const_cast<fmmbem_ctx*>(c), c->opt.direct != 0 || c->tree.L < 2);
+  *out = c->last;
+  return FMMBEM_OK;
+  API_END
+}
+
+fmmbem_status fmmbem_tree_info_get(const fmmbem_ctx* c, fmmbem_tree_info* o) {
+  if (!c || !o) return FMMBEM_E_INVALID;
+  o->levels = c->tree.L;
+  o->n_leaves = c->tree.n_leaves;
+  o->n_cells = c->tree.n_cells;
+  o->n_panels = c->np;
+  o->n_charges = c->nc;
+  o->nbr_pairs = c->tree.nbr_pairs;
+  o->m2l_pairs = c->tree.m2l_pairs;
+  o->root_width = c->tree.W;
+  for (int d = 0; d < 3; ++d) o->root_origin[d] = c->tree.x0[d];
+  return FMMBEM_OK;
+}
+
+}  // extern "C"

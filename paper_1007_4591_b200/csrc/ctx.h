@@ -1,0 +1,80 @@
+// ctx.h -- internal state of one fmmbem_ctx (CUDA path).
+#pragma once
+#include <array>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace fmm {
+
+// Points of one kind in leaf (Morton) order.  pos.xyz = coordinates relative to the
+// centre of the point's leaf (FP32), pos.w = per-point weight factor
+// (panel area * quadrature weight for sources; charge q for charges).
+struct PointSet {
+  int64_t n = 0;
+  DevBuf<float4> pos;
+  DevBuf<float4> nrm;   // unit normals (panel targets only)
+  DevBuf<int> leaf;     // leaf index of each point
+  DevBuf<int> begin;    // [n_leaves + 1] CSR of points per leaf
+  DevBuf<int> cell_cnt; // [n_cells] number of points in each cell's subtree
+  int div = 1;          // the x-vector index of point j is j / div (K for quadrature sources)
+};
+
+struct Tree {
+  int L = 0;                  // leaf level (root = 0)
+  double x0[3] = {0, 0, 0};   // root cube min corner
+  double W = 1.0;             // root cube width (8-bit mantissa -> exact integer*h in FP32)
+  int64_t n_leaves = 0, n_cells = 0;
+  std::vector<int64_t> lvl_off;  // [L + 2] first global cell index per level (level-major)
+  DevBuf<uint64_t> key;          // [n_cells] Morton key at the cell's level
+  DevBuf<int> parent;            // [n_cells] global parent index (-1 at the root)
+  DevBuf<int> child_begin, child_end;  // [n_cells] global child range (level + 1)
+  DevBuf<int4> leaf_ijk;         // [n_leaves] integer leaf coordinates
+  DevBuf<int> nbr_off, nbr_idx;  // leaf-level neighbour CSR (leaf indices, incl. self)
+  DevBuf<int> m2l_off, m2l_idx;  // [n_cells+1] interaction-list CSR (global source cell idx)
+  int64_t nbr_pairs = 0, m2l_pairs = 0;
+  double width(int l) const { return W / (double)(1LL << l); }
+};
+
+struct Timing {
+  cudaEvent_t ev[12];
+  bool valid = false;
+};
+
+}  // namespace fmm
+
+struct fmmbem_ctx {
+  fmmbem_options opt{};
+  int P = 10, K = 1, NC = 55;  // terms, quadrature points, complex coefficients per expansion
+  double eps_in = 4, eps_out = 80, f = 0, eps_hat = 0;
+  int64_t np = 0, nc = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;  // internal stream for setup / host-buffer calls
+
+  fmm::Tree tree;
+  fmm::PointSet pan;   // panels: targets (centroid + normal); sources when K == 1
+  fmm::PointSet quad;  // quadrature points (K > 1), panel-major within each leaf
+  fmm::PointSet chg;   // charges
+  std::vector<int64_t> pan_ids;     // local -> caller triangle index
+  fmm::DevBuf<int> chg_ids;         // local charge -> caller charge index
+
+  fmm::DevBuf<float2> Mx, Lx;       // expansions [n_cells * NC]
+  fmm::DevBuf<float2> Itab;         // M2L irregular-harmonic table [343 * NI]
+  int NI = 0;
+  fmm::DevBuf<float> tmp_x, tmp_y;  // host-buffer matvec staging / scratch
+  fmm::DevBuf<float> En, psi;       // charge fields (cached)
+  bool have_fields = false;
+  fmm::DevBuf<int> flag;            // device error flags
+  fmm::DevBuf<double> red;          // reduction scratch
+
+  // GMRES workspace
+  fmm::DevBuf<float> V;     // [(m+1) * np]
+  fmm::DevBuf<float> w;     // [np]
+  fmm::DevBuf<double> hd;   // [m+2]
+  fmm::DevBuf<double> part; // partial sums [blocks * (m+2)]
+
+  int64_t p2p_inter_kp = 0, p2p_inter_chg = 0;  // exact interaction counts
+  int64_t m2l_pairs_kp = 0;
+  fmmbem_timing last{};
+  cudaEvent_t ev[10] = {};
+};

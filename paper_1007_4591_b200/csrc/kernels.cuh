@@ -1,0 +1,57 @@
+// kernels.cuh -- launch interfaces shared by the .cu files of libfmmbem.
+#pragma once
+#include "ctx.h"
+
+namespace fmm {
+
+// y[i] = ax * x[i] + b * raw[i]   (x may be null)  -- or, for accumulate = true, y[i] += b * raw[i]
+struct OutArg {
+  float* y = nullptr;
+  const float* x = nullptr;
+  float ax = 0.f;
+  float b = 1.f;
+};
+
+// A source set for one apply: weight of point j = (x ? x[j / div] : 1) * pos[j].w
+struct SrcArg {
+  const PointSet* set = nullptr;
+  const float* x = nullptr;
+};
+
+// targets: positions (+ normals for normal-derivative outputs)
+struct TgtArg {
+  const PointSet* set = nullptr;
+};
+
+struct Outputs {
+  OutArg pot;  // potential  phi = sum w / r                (raw, before b)
+  OutArg dn;   // normal derivative n . grad phi             (raw, before b)
+};
+
+void build_tree(fmmbem_ctx* c, const double* cen, const double* nrm, const double* area, const double* qpts,
+                const double* wq, const double* cxyz, const double* cq, cudaStream_t s);
+
+// near field; writes y = ax x + b raw (overwrites)
+void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
+                bool direct, cudaStream_t st);
+// exact interaction count of launch_p2p(t, s) (list mode) -- setup-time helper
+int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct);
+
+// far field (expansions in c->Mx / c->Lx); l2p accumulates y += b far
+void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
+void launch_m2l(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStream_t st);
+void launch_downward(fmmbem_ctx* c, const PointSet& tgt, cudaStream_t st);
+void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t st);
+void init_tables(fmmbem_ctx* c);
+
+// Krylov / reductions
+double dot_weighted(fmmbem_ctx* c, int64_t n, const float* a, const float* b, const float4* w_area,
+                    cudaStream_t s);
+fmmbem_status gmres_solve(fmmbem_ctx* c, const float* b, float* x, double tol, int restart, int max_iters,
+                          const float* x0, double* hist, int* iters, double* relres, cudaStream_t s);
+
+// one full FMM (or direct) evaluation of targets t from sources s
+void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
+              cudaStream_t st, bool timing);
+
+}  // namespace fmm

@@ -1,0 +1,199 @@
+"""Parity of the CUDA path (through the C ABI) with the FP64 oracle, element by element.
+
+Tolerances:
+  * direct mode (all-pairs P2P, FP32): rel L2 <= 2e-5 (FP32 recursive sums of N ~ 10^4 random-sign
+    terms: ~sqrt(N) u sum|t|/|sum t| with u = 6e-8 and sum|t|/|sum t| ~ 10-30)
+  * FMM matvec: rel L2 <= 1e-4 (BASELINE north_star) at the chosen expansion order
+  * energies: <= 1e-3 relative to the oracle (BASELINE north_star)
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import bem  # noqa: E402
+from synth import configs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def solver(cfg, **kw):
+    from paper_1007_4591_b200 import Solver
+    return Solver.from_config(cfg, **kw)
+
+
+def run(s, x_global, op):
+    y = s.matvec(torch.tensor(s.to_local(x_global), dtype=torch.float32, device="cuda"), op)
+    torch.cuda.synchronize()
+    return s.to_global(y.cpu().numpy().astype(np.float64))
+
+
+def ref_op(P, x, op):
+    if op == "kprime":
+        return bem.apply_kprime(P.pan, x)
+    if op == "single":
+        return bem.apply_single(P.pan, x)
+    return bem.apply_A(P.pan, x, P.f)
+
+
+CASES = {
+    "born8": lambda: configs.born(8),
+    "kirk12": lambda: configs.kirkwood(12),
+    "kirk24": lambda: configs.kirkwood(24),
+    "lyso20": lambda: configs.lysozyme(nu=20, n_atoms=200),
+}
+
+
+@pytest.fixture(scope="module")
+def problems():
+    return {k: (f(), bem.Problem(f())) for k, f in CASES.items()}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("op", ["kprime", "single", "A"])
+def test_direct_mode_matches_oracle(problems, case, op):
+    cfg, P = problems[case]
+    s = solver(cfg, direct=1)
+    x = np.random.default_rng(1).normal(size=P.pan.n)
+    err = bem.rel_l2(run(s, x, op), ref_op(P, x, op))
+    assert err < 2e-5, err
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("op", ["kprime", "single", "A"])
+def test_fmm_matvec_matches_oracle(problems, case, op):
+    cfg, P = problems[case]
+    s = solver(cfg, terms=12, leaf_points=16)
+    info = s.tree_info()
+    assert info["levels"] >= 2
+    x = np.random.default_rng(2).normal(size=P.pan.n)
+    err = bem.rel_l2(run(s, x, op), ref_op(P, x, op))
+    assert err < 1e-4, (err, info)
+
+
+def test_fmm_error_decreases_with_terms(problems):
+    cfg, P = problems["kirk24"]
+    x = np.random.default_rng(3).normal(size=P.pan.n)
+    ref = ref_op(P, x, "kprime")
+    errs = []
+    for p in (4, 6, 8, 10, 12, 14):
+        s = solver(cfg, terms=p, leaf_points=16)
+        errs.append(bem.rel_l2(run(s, x, "kprime"), ref))
+    assert all(b < a for a, b in zip(errs, errs[1:4])), errs
+    assert errs[-1] < 3e-5, errs
+
+
+@pytest.mark.parametrize("K", [3, 6, 7])
+def test_quadrature_rules_match_oracle(K):
+    cfg = configs.kirkwood(10)
+    P = bem.Problem(cfg, K=K)
+    x = np.random.default_rng(4).normal(size=P.pan.n)
+    for direct, tol in ((1, 2e-5), (0, 1e-4)):
+        s = solver(cfg, quad_points=K, direct=direct, terms=12, leaf_points=16)
+        for op in ("kprime", "single"):
+            err = bem.rel_l2(run(s, x, op), ref_op(P, x, op))
+            assert err < tol, (K, direct, op, err)
+    s = solver(cfg, quad_points=K, terms=12, leaf_points=16)
+    r = s.solve()
+    ref = P.solve("gmres")
+    assert abs(r["dG"] / ref["dG"] - 1) < 1e-3
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_charge_fields_match_oracle(problems, case):
+    cfg, P = problems[case]
+    s = solver(cfg, terms=12, leaf_points=16)
+    En, psi = s.charge_fields()
+    En = s.to_global(En.cpu().numpy().astype(np.float64))
+    psi = s.to_global(psi.cpu().numpy().astype(np.float64))
+    assert bem.rel_l2(En, P.E) < 1e-4
+    y, owner, aw = P.pan.sources()
+    from oracle import _cdirect
+    psi_ref = _cdirect.pot_sum(P.pan.centroid, None, P.cxyz, P.cq, None)
+    assert bem.rel_l2(psi, psi_ref) < 1e-4
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_solve_and_bibee_energies_match_oracle(problems, case):
+    cfg, P = problems[case]
+    s = solver(cfg, terms=12, leaf_points=16)
+    r = s.solve()
+    ref = P.solve("gmres")
+    assert r["converged"] and abs(r["dG"] / ref["dG"] - 1) < 1e-3, (r["dG"], ref["dG"])
+    assert abs(r["iterations"] - ref["iterations"]) <= 2
+    sig = s.to_global(r["sigma"].cpu().numpy().astype(np.float64))
+    assert bem.rel_l2(sig, ref["sigma"]) < 1e-3
+    h = r["history"]
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(h, h[1:]))
+    for v in ("cfa", "p", "lb"):
+        e = s.bibee(v)["dG"]
+        e_ref = P.bibee(v)["dG"]
+        assert abs(e / e_ref - 1) < 1e-3, (v, e, e_ref)
+    # reaction potential (plain C sigma form, Eq. 5) against the oracle's
+    phi = s.reaction_potential(r["sigma"])
+    phi_ref = bem.reaction_potential(P.pan, sig, P.cxyz)
+    assert bem.rel_l2(phi, phi_ref) < 1e-3
+
+
+def test_born_discrete_pin_within_1e5():
+    """config 1 must reproduce the discrete Born energy -0.00982207 within 1e-5."""
+    s = solver(configs.born(8), direct=1)
+    r = s.solve()
+    assert abs(r["dG"] / -0.00982207 - 1) < 1e-5, r["dG"]
+    assert r["iterations"] == 4
+
+
+def test_matvec_is_deterministic_and_linear(problems):
+    cfg, P = problems["kirk24"]
+    s = solver(cfg, terms=10, leaf_points=16)
+    rng = np.random.default_rng(5)
+    a, b = rng.normal(size=P.pan.n), rng.normal(size=P.pan.n)
+    ya, yb = run(s, a, "kprime"), run(s, b, "kprime")
+    assert np.array_equal(ya, run(s, a, "kprime"))
+    yab = run(s, 2 * a + 3 * b, "kprime")
+    assert bem.rel_l2(yab, 2 * ya + 3 * yb) < 1e-6
+
+
+def test_translation_invariance(problems):
+    cfg, P = problems["kirk12"]
+    cfg2 = dict(cfg, vertices=cfg["vertices"] + [17.3, -4.1, 9.0], charge_xyz=cfg["charge_xyz"] + [17.3, -4.1, 9.0])
+    x = np.random.default_rng(6).normal(size=P.pan.n)
+    y1 = run(solver(cfg, terms=12, leaf_points=16), x, "kprime")
+    y2 = run(solver(cfg2, terms=12, leaf_points=16), x, "kprime")
+    assert bem.rel_l2(y2, y1) < 2e-4
+
+
+def test_error_statuses():
+    from paper_1007_4591_b200 import FmmbemError
+    v = np.array([[0.0, 0, 0], [1, 0, 0], [2, 0, 0], [0, 1, 0]])
+    with pytest.raises(FmmbemError, match="E_DEGENERATE.*degenerate triangle 1"):
+        solver(dict(vertices=v, triangles=np.array([[0, 1, 3], [0, 1, 2]]), charge_xyz=np.zeros((0, 3)),
+                    charge_q=np.zeros(0), eps_in=4.0, eps_out=80.0))
+    with pytest.raises(FmmbemError, match="E_DEGENERATE.*out of range"):
+        solver(dict(vertices=v, triangles=np.array([[0, 1, 7]]), charge_xyz=np.zeros((0, 3)),
+                    charge_q=np.zeros(0), eps_in=4.0, eps_out=80.0))
+    cfg = configs.born(4)
+    with pytest.raises(FmmbemError, match="E_INVALID"):
+        solver(dict(cfg, eps_out=4.0))
+    with pytest.raises(FmmbemError, match="E_INVALID"):
+        solver(cfg, terms=40)
+    # a charge exactly on a centroid
+    P = bem.Panels(cfg["vertices"], cfg["triangles"])
+    bad = dict(cfg, charge_xyz=P.centroid[5:6].copy(), charge_q=np.ones(1))
+    s = solver(bad, direct=1)
+    with pytest.raises(FmmbemError, match="E_COINCIDENT"):
+        s.bibee("cfa")
+    # duplicate triangle -> duplicate centroid
+    dup = dict(cfg, triangles=np.concatenate([cfg["triangles"], cfg["triangles"][:1]]))
+    with pytest.raises(FmmbemError, match="E_COINCIDENT"):
+        solver(dup)
+
+
+def test_single_panel_and_no_charges():
+    v = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0]])
+    cfg = dict(vertices=v, triangles=np.array([[0, 1, 2]]), charge_xyz=np.zeros((0, 3)), charge_q=np.zeros(0),
+               eps_in=4.0, eps_out=80.0)
+    s = solver(cfg)
+    y = run(s, np.ones(1), "kprime")
+    assert y[0] == 0.0  # self excluded
+    assert s.bibee("cfa")["dG"] == 0.0
