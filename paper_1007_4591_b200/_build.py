@@ -1,6 +1,10 @@
-"""Build libfmmbem.so in-tree for sm_100a (nvcc; no JIT cache, no torch extension)."""
+"""Build libfmmbem.so in-tree for sm_100a (nvcc; no JIT cache, no torch extension).
+
+Each .cu is compiled to an object in parallel (build/), then linked into libfmmbem.so.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import glob
 import os
 import subprocess
@@ -10,34 +14,52 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfmmbem.so")
 INC = os.path.join(os.path.dirname(HERE), "include")
+OBJ = os.path.join(os.path.dirname(HERE), "build", "obj")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-              "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared", "--expt-relaxed-constexpr"]
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
 
 
 def sources():
     return sorted(glob.glob(os.path.join(SRC, "*.cu")))
 
 
-def deps():
-    return sources() + sorted(glob.glob(os.path.join(SRC, "*.cuh")) + glob.glob(os.path.join(SRC, "*.h"))
-                              + glob.glob(os.path.join(INC, "*.h")))
+def headers():
+    return sorted(glob.glob(os.path.join(SRC, "*.cuh")) + glob.glob(os.path.join(SRC, "*.h"))
+                  + glob.glob(os.path.join(INC, "*.h")))
+
+
+def _obj(src):
+    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
 
 
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(f) > t for f in deps())
+    return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
 def build(force: bool = False, verbose: bool = True, extra=()) -> str:
     if not force and not needs_build():
         return LIB
-    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", INC, "-o", LIB + ".tmp", *sources(), "-lcudart"]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
+    os.makedirs(OBJ, exist_ok=True)
+    hdr_t = max(os.path.getmtime(f) for f in headers())
+
+    def compile_one(src):
+        o = _obj(src)
+        if not force and os.path.exists(o) and os.path.getmtime(o) > max(os.path.getmtime(src), hdr_t):
+            return o
+        cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", INC, "-c", src, "-o", o]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        return o
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp", *objs, "-lcudart"]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     return LIB

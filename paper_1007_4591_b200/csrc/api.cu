@@ -2,6 +2,7 @@
 // evaluation.  Every step of the path runs in this library's kernels;
 // the host only validates, launches and runs the small FP64 GMRES least-squares problem.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -309,6 +310,7 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   FMM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
   c->P = opt.terms;
+  if (const char* e = std::getenv("FMMBEM_M2L")) c->m2l_mode = (std::string(e) == "p4") ? 1 : 0;
   c->NC = c->P * (c->P + 1) / 2;
   c->K = opt.quad_points;
   c->eps_in = eps_in;

@@ -1,6 +1,7 @@
 // ctx.h -- internal state of one fmmbem_ctx (CUDA path).
 #pragma once
 #include <array>
+#include <memory>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -34,6 +35,16 @@ struct Tree {
   DevBuf<int> m2l_off, m2l_idx;  // [n_cells+1] interaction-list CSR (global source cell idx)
   int64_t nbr_pairs = 0, m2l_pairs = 0;
   double width(int l) const { return W / (double)(1LL << l); }
+};
+
+// compacted M2L work for one (source set, target set) pair: rows = target cells
+struct M2LWork {
+  const PointSet* src = nullptr;
+  const PointSet* tgt = nullptr;
+  int64_t pairs = 0, rows = 0;
+  DevBuf<int> idx;   // [pairs] source cells
+  DevBuf<int> cell;  // [rows] target cells
+  DevBuf<int> off;   // [rows + 1]
 };
 
 struct Timing {
@@ -73,6 +84,8 @@ struct fmmbem_ctx {
   fmm::DevBuf<double> hd;   // [m+2]
   fmm::DevBuf<double> part; // partial sums [blocks * (m+2)]
 
+  std::vector<std::unique_ptr<fmm::M2LWork>> m2l_cache;
+  int m2l_mode = 0;  // 0 = rotation O(P^3) when available, 1 = plain O(P^4)
   int64_t p2p_inter_kp = 0, p2p_inter_chg = 0;  // exact interaction counts
   int64_t m2l_pairs_kp = 0;
   fmmbem_timing last{};

@@ -435,6 +435,11 @@ void launch_m2l(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStr
   const int L = T.L, P = c->P;
   if (L < 2) return;
   c->Lx.zero(st);
+  if (c->m2l_mode == 0 && rot_supported(P)) {
+    init_rot_tables();
+    launch_m2l_rot(c, m2l_work(c, src, tgt, st), st);
+    return;
+  }
   const int n = (int)(T.n_cells - T.lvl_off[2]);
   const size_t smem = (size_t)M2L_SB * (P * P + (2 * P - 1) * (2 * P - 1)) * sizeof(float2);
   static bool attr = false;

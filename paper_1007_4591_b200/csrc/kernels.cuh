@@ -44,6 +44,13 @@ void launch_downward(fmmbem_ctx* c, const PointSet& tgt, cudaStream_t st);
 void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t st);
 void init_tables(fmmbem_ctx* c);
 
+// rotation-accelerated M2L (m2l_rot.cu)
+bool rot_supported(int P);
+void init_rot_tables();
+const M2LWork& m2l_work(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStream_t st);
+void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st);
+void scan_ints(const int* in, int* out, int n, cudaStream_t s);  // exclusive
+
 // Krylov / reductions
 double dot_weighted(fmmbem_ctx* c, int64_t n, const float* a, const float* b, const float4* w_area,
                     cudaStream_t s);

@@ -1,0 +1,389 @@
+// m2l_rot.cu -- rotation-accelerated M2L, O(P^3) per translation ("spherical
+// harmonic rotations are performed before each translation at O(p^3) cost").
+//
+// For a source cell s and target cell t at offset delta = (c_t - c_s)/w = rho (sin t cos p,
+// sin t sin p, cos t), the scaled translation L~ = T(delta) M~ (farfield.cu header) is factored
+//   M' = Phi(-pi/2) D Phi(t) D^-1 Phi(p + pi/2) M          (rotate delta onto +z)
+//   L' = Tz(rho) M',   L'_j^k = (-1)^{j+k} sum_{n>=k} M'_n^k (j+n)! / rho^{j+n+1}   (coaxial)
+//   L  = Phi(-pi/2 - p) D^-T Phi(-t) D^T Phi(pi/2) L'       (rotate back)
+// where Phi(a) = diag(e^{i m a}) and D = W(Ry(pi/2)), D^-1 = W(Ry(-pi/2)) are FIXED real
+// matrices per degree (R_n(Q v) = W^n(Q) R_n(v)); in this basis W^n(Ry(b)) = diag(1/f) d^n(b)
+// diag(f), f_m = sqrt((n+m)!(n-m)!), d^n = Wigner's small d.  Ry(t) = S Rz(t) S^-1 with
+// S = Rz(pi/2) Ry(pi/2) is what lets one pair of fixed matrices serve every direction.  The two
+// Phi(+-pi/2) around Tz cancel (Tz is diagonal in the order k).  Vectors of a real field are
+// conjugate symmetric, so each real matrix X acts on the stored m >= 0 half as
+//   Re b_m' = sum_{m>=0} E_m'm Re a_m,  Im b_m' = sum_{m>0} F_m'm Im a_m,
+//   E_m'm = X_m'm + (-1)^m X_m',-m,  F_m'm = X_m'm - (-1)^m X_m',-m   (E_m'0 = X_m'0, F_m'0 = 0)
+// i.e. 2 (n+1)^2 FMAs per degree.  One thread owns one (target, source) pair; the whole pipeline
+// is unrolled at compile time (P is a template parameter) with the E/F tables in constant
+// memory, uniform across the warp, so they enter FFMAs as constant-bank operands.  Each thread's
+// working vector lives in a private shared-memory slot and streams through registers one degree
+// block (rotations) or one order column (coaxial translation) at a time, so registers stay low for
+// any P.  The 32 pairs of a warp belong to one target cell and are summed through the same slots.
+#include <cmath>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace fmm {
+
+namespace {
+
+constexpr int RMAX = 16;  // degrees covered by the rotation tables
+__host__ __device__ constexpr int tri3(int n) { return n * (n + 1) * (2 * n + 1) / 6; }  // sum_{k<n} (k+1)^2
+constexpr int TSZ = tri3(RMAX);
+// [matrix][E/F][degree block]: 0 = D^-1, 1 = D, 2 = D^T, 3 = D^-T
+__constant__ float c_rot[4][2][TSZ];
+
+__host__ __device__ constexpr float factf(int n) {
+  float f = 1.f;
+  for (int i = 2; i <= n; ++i) f *= (float)i;
+  return f;
+}
+
+// Per-thread vector slot in shared memory, coefficient-major / lane-minor ([2*NC][33]): all lanes
+// touch the same coefficient at once -> conflict-free; the 33 stride keeps the final per-row
+// reduction conflict-free too.
+struct Slot {
+  float* base;  // &sv[0][lane]
+  __device__ __forceinline__ float& re(int c) const { return base[(2 * c) * 33]; }
+  __device__ __forceinline__ float& im(int c) const { return base[(2 * c + 1) * 33]; }
+};
+
+// one degree block: b = X a (E/F form), a and b in registers
+template <int n, int X>
+__device__ __forceinline__ void mat_block(const float (&ar)[n + 1], const float (&ai)[n + 1], float (&br)[n + 1],
+                                          float (&bi)[n + 1]) {
+#pragma unroll
+  for (int mp = 0; mp <= n; ++mp) {
+    float re = 0.f, im = 0.f;
+#pragma unroll
+    for (int m = 0; m <= n; ++m) {
+      re = fmaf(c_rot[X][0][tri3(n) + mp * (n + 1) + m], ar[m], re);
+      if (m > 0) im = fmaf(c_rot[X][1][tri3(n) + mp * (n + 1) + m], ai[m], im);
+    }
+    br[mp] = re;
+    bi[mp] = im;
+  }
+}
+
+// (r + i s) *= (zr + i zi)
+__device__ __forceinline__ void cmul_ip(float& r, float& s, float zr, float zi) {
+  float t = r * zr - s * zi;
+  s = r * zi + s * zr;
+  r = t;
+}
+
+// M' block n = rho^-n D Phi(t) D^-1 Phi(p + pi/2) M_n
+template <int P, int n>
+__device__ __forceinline__ void pass_a(const Slot& sl, const float2* __restrict__ Ms, const float (&zar)[P],
+                                       const float (&zai)[P], const float (&zbr)[P], const float (&zbi)[P],
+                                       float scale, float irho) {
+  constexpr int c0 = n * (n + 1) / 2;
+  float ar[n + 1], ai[n + 1], br[n + 1], bi[n + 1];
+#pragma unroll
+  for (int m = 0; m <= n; ++m) {
+    float2 q = __ldg(Ms + c0 + m);
+    ar[m] = q.x;
+    ai[m] = q.y;
+    if (m > 0) cmul_ip(ar[m], ai[m], zar[m], zai[m]);  // Phi(p + pi/2)
+  }
+  mat_block<n, 0>(ar, ai, br, bi);                    // D^-1
+#pragma unroll
+  for (int m = 1; m <= n; ++m) cmul_ip(br[m], bi[m], zbr[m], zbi[m]);  // Phi(t)
+  mat_block<n, 1>(br, bi, ar, ai);                    // D
+#pragma unroll
+  for (int m = 0; m <= n; ++m) {
+    sl.re(c0 + m) = ar[m] * scale;
+    sl.im(c0 + m) = ai[m] * scale;
+  }
+  if constexpr (n + 1 < P) pass_a<P, n + 1>(sl, Ms, zar, zai, zbr, zbi, scale * irho, irho);
+}
+
+// coaxial translation of order column k (input scaled by rho^-n, output missing rho^-(j+1))
+template <int P, int k>
+__device__ __forceinline__ void pass_b(const Slot& sl) {
+  float tr[P - k], ti[P - k];
+#pragma unroll
+  for (int n = k; n < P; ++n) {
+    tr[n - k] = sl.re(n * (n + 1) / 2 + k);
+    ti[n - k] = sl.im(n * (n + 1) / 2 + k);
+  }
+#pragma unroll
+  for (int j = k; j < P; ++j) {
+    float re = 0.f, im = 0.f;
+#pragma unroll
+    for (int n = k; n < P; ++n) {
+      re = fmaf(factf(j + n), tr[n - k], re);
+      im = fmaf(factf(j + n), ti[n - k], im);
+    }
+    const float sg = ((j + k) & 1) ? -1.f : 1.f;
+    sl.re(j * (j + 1) / 2 + k) = sg * re;
+    sl.im(j * (j + 1) / 2 + k) = sg * im;
+  }
+  if constexpr (k + 1 < P) pass_b<P, k + 1>(sl);
+}
+
+// L block j = Phi(-p - pi/2) D^-T Phi(-t) D^T rho^-(j+1) L'_j
+template <int P, int n>
+__device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], const float (&zai)[P],
+                                       const float (&zbr)[P], const float (&zbi)[P], float scale, float irho) {
+  constexpr int c0 = n * (n + 1) / 2;
+  float ar[n + 1], ai[n + 1], br[n + 1], bi[n + 1];
+#pragma unroll
+  for (int m = 0; m <= n; ++m) {
+    ar[m] = sl.re(c0 + m) * scale;
+    ai[m] = sl.im(c0 + m) * scale;
+  }
+  mat_block<n, 2>(ar, ai, br, bi);                    // D^T
+#pragma unroll
+  for (int m = 1; m <= n; ++m) cmul_ip(br[m], bi[m], zbr[m], -zbi[m]);  // Phi(-t)
+  mat_block<n, 3>(br, bi, ar, ai);                    // D^-T
+#pragma unroll
+  for (int m = 0; m <= n; ++m) {
+    if (m > 0) cmul_ip(ar[m], ai[m], zar[m], -zai[m]);  // Phi(-p - pi/2)
+    sl.re(c0 + m) = ar[m];
+    sl.im(c0 + m) = ai[m];
+  }
+  if constexpr (n + 1 < P) pass_c<P, n + 1>(sl, zar, zai, zbr, zbi, scale * irho, irho);
+}
+
+template <int P>
+__global__ void __launch_bounds__(32) k_m2l_rot(const int* __restrict__ tcells, const int* __restrict__ off,
+                                                const int* __restrict__ idx, const uint64_t* __restrict__ key,
+                                                const float2* __restrict__ M, float2* __restrict__ Lx) {
+  constexpr int NC = P * (P + 1) / 2;
+  constexpr int NR = (NC + 31) / 32;
+  __shared__ float sv[2 * NC * 33];
+  const int cell = tcells[blockIdx.x];
+  const int lo = off[blockIdx.x], hi = off[blockIdx.x + 1];
+  const int lane = threadIdx.x;
+  const Slot sl{sv + lane};
+  int tx, ty, tz;
+  demorton(key[cell], tx, ty, tz);
+  float2 acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = make_float2(0.f, 0.f);
+  for (int e0 = lo; e0 < hi; e0 += 32) {
+    const int e = e0 + lane;
+    if (e < hi) {
+      const int s = idx[e];
+      int sx, sy, sz;
+      demorton(key[s], sx, sy, sz);
+      const float dx = (float)(tx - sx), dy = (float)(ty - sy), dz = (float)(tz - sz);
+      const float rxy2 = dx * dx + dy * dy;
+      const float rxy = sqrtf(rxy2);
+      const float irho = rsqrtf(rxy2 + dz * dz);
+      float cp = 1.f, sp = 0.f;
+      if (rxy > 0.f) {
+        cp = dx / rxy;
+        sp = dy / rxy;
+      }
+      // powers of za = e^{i(p + pi/2)} = i e^{ip} and zb = e^{it}
+      float zar[P], zai[P], zbr[P], zbi[P];
+      zar[0] = 1.f;
+      zai[0] = 0.f;
+      zbr[0] = 1.f;
+      zbi[0] = 0.f;
+      const float ar1 = -sp, ai1 = cp, br1 = dz * irho, bi1 = rxy * irho;
+#pragma unroll
+      for (int m = 1; m < P; ++m) {
+        zar[m] = zar[m - 1] * ar1 - zai[m - 1] * ai1;
+        zai[m] = zar[m - 1] * ai1 + zai[m - 1] * ar1;
+        zbr[m] = zbr[m - 1] * br1 - zbi[m - 1] * bi1;
+        zbi[m] = zbr[m - 1] * bi1 + zbi[m - 1] * br1;
+      }
+      pass_a<P, 0>(sl, M + (size_t)s * NC, zar, zai, zbr, zbi, 1.f, irho);
+      pass_b<P, 0>(sl);
+      pass_c<P, 0>(sl, zar, zai, zbr, zbi, irho, irho);
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        sl.re(c) = 0.f;
+        sl.im(c) = 0.f;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int c = lane + 32 * r;
+      if (c < NC) {
+        float sx = 0.f, sy = 0.f;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) {
+          sx += sv[(2 * c) * 33 + l];
+          sy += sv[(2 * c + 1) * 33 + l];
+        }
+        acc[r].x += sx;
+        acc[r].y += sy;
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int c = lane + 32 * r;
+    if (c < NC) {
+      float2 o = Lx[(size_t)cell * NC + c];
+      o.x += acc[r].x;
+      o.y += acc[r].y;
+      Lx[(size_t)cell * NC + c] = o;
+    }
+  }
+}
+
+// Wigner small d^n_{m'm}(b) (explicit sum)
+double wigner_d(int n, int mp, int m, double b) {
+  auto fact = [](int k) {
+    double f = 1;
+    for (int i = 2; i <= k; ++i) f *= i;
+    return f;
+  };
+  int s0 = std::max(0, m - mp), s1 = std::min(n + m, n - mp);
+  double t = 0, c = std::cos(b / 2), s = std::sin(b / 2);
+  for (int k = s0; k <= s1; ++k) {
+    double sg = ((mp - m + k) & 1) ? -1.0 : 1.0;
+    t += sg / (fact(n + m - k) * fact(k) * fact(mp - m + k) * fact(n - mp - k)) * std::pow(c, 2 * n + m - mp - 2 * k) *
+         std::pow(s, mp - m + 2 * k);
+  }
+  return t * std::sqrt(fact(n + mp) * fact(n - mp) * fact(n + m) * fact(n - m));
+}
+
+// compacted interaction lists (sources with points of `src`, targets with points of `tgt`)
+__global__ void k_compact_count(int n, int cell_off, const int* __restrict__ off, const int* __restrict__ idx,
+                                const int* __restrict__ scnt, const int* __restrict__ tcnt, int* cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = cell_off + i;
+  int m = 0;
+  if (tcnt[c] > 0)
+    for (int e = off[c]; e < off[c + 1]; ++e) m += scnt[idx[e]] > 0;
+  cnt[i] = m;
+}
+
+__global__ void k_compact_fill(int n, int cell_off, const int* __restrict__ off, const int* __restrict__ idx,
+                               const int* __restrict__ scnt, const int* __restrict__ pos, int* out_idx,
+                               int* out_cell, int* out_off) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = cell_off + i;
+  const int start = pos[i], end = pos[i + 1];
+  if (start == end) return;
+  int w = start;
+  for (int e = off[c]; e < off[c + 1]; ++e)
+    if (scnt[idx[e]] > 0) out_idx[w++] = idx[e];
+  // row r of the compacted list = number of non-empty rows before i
+  out_cell[pos[n + 1 + i]] = c;
+  out_off[pos[n + 1 + i]] = start;
+}
+
+__global__ void k_row_flags(int n, const int* __restrict__ cnt, int* flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = cnt[i] > 0;
+}
+
+}  // namespace
+
+// instantiated orders (others use the O(P^4) kernel in farfield.cu)
+bool rot_supported(int P) { return P == 8 || P == 10 || P == 12; }
+
+void init_rot_tables() {
+  static bool done = false;
+  if (done) return;
+  std::vector<float> h(4 * 2 * TSZ, 0.f);
+  for (int n = 0; n < RMAX; ++n) {
+    std::vector<double> f(2 * n + 1);
+    for (int m = -n; m <= n; ++m) {
+      double a = 1, b = 1;
+      for (int i = 2; i <= n + m; ++i) a *= i;
+      for (int i = 2; i <= n - m; ++i) b *= i;
+      f[m + n] = std::sqrt(a * b);
+    }
+    // W(+pi/2) = D, W(-pi/2) = D^-1 in the R_n^m basis
+    auto W = [&](int mp, int m, double beta) { return wigner_d(n, mp, m, beta) * f[m + n] / f[mp + n]; };
+    for (int X = 0; X < 4; ++X) {
+      for (int mp = 0; mp <= n; ++mp)
+        for (int m = 0; m <= n; ++m) {
+          // X_{mp,m} for X in {D^-1, D, D^T, D^-T}
+          auto Xv = [&](int a, int b) {
+            switch (X) {
+              case 0: return W(a, b, -M_PI / 2);
+              case 1: return W(a, b, M_PI / 2);
+              case 2: return W(b, a, M_PI / 2);
+              default: return W(b, a, -M_PI / 2);
+            }
+          };
+          double e, g;
+          if (m == 0) {
+            e = Xv(mp, 0);
+            g = 0;
+          } else {
+            double sg = (m & 1) ? -1.0 : 1.0;
+            e = Xv(mp, m) + sg * Xv(mp, -m);
+            g = Xv(mp, m) - sg * Xv(mp, -m);
+          }
+          h[(X * 2 + 0) * TSZ + tri3(n) + mp * (n + 1) + m] = (float)e;
+          h[(X * 2 + 1) * TSZ + tri3(n) + mp * (n + 1) + m] = (float)g;
+        }
+    }
+  }
+  FMM_CUDA(cudaMemcpyToSymbol(c_rot, h.data(), h.size() * sizeof(float)));
+  done = true;
+}
+
+// Build (or fetch) the compacted M2L work list for (src, tgt): rows = target cells at levels >= 2
+// with target points and at least one source cell holding source points.
+const M2LWork& m2l_work(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStream_t st) {
+  for (auto& w : c->m2l_cache)
+    if (w->src == &src && w->tgt == &tgt) return *w;
+  const Tree& T = c->tree;
+  auto w = std::make_unique<M2LWork>();
+  w->src = &src;
+  w->tgt = &tgt;
+  const int off0 = (int)T.lvl_off[2];
+  const int n = (int)(T.n_cells - off0);
+  DevBuf<int> cnt, pos;
+  cnt.alloc(2 * (n + 1));
+  pos.alloc(2 * (n + 1));
+  cnt.zero(st);
+  k_compact_count<<<ceil_div(n, 256), 256, 0, st>>>(n, off0, T.m2l_off.get(), T.m2l_idx.get(), src.cell_cnt.get(),
+                                                     tgt.cell_cnt.get(), cnt.get());
+  k_row_flags<<<ceil_div(n, 256), 256, 0, st>>>(n, cnt.get(), cnt.get() + n + 1);
+  FMM_CHECK_LAUNCH();
+  scan_ints(cnt.get(), pos.get(), n + 1, st);                    // pair offsets
+  scan_ints(cnt.get() + n + 1, pos.get() + n + 1, n + 1, st);    // row ids
+  int h[2] = {0, 0};
+  FMM_CUDA(cudaMemcpyAsync(&h[0], pos.get() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(&h[1], pos.get() + 2 * n + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  w->pairs = h[0];
+  w->rows = h[1];
+  w->idx.alloc(std::max(1, h[0]));
+  w->cell.alloc(std::max(1, h[1]));
+  w->off.alloc(h[1] + 1);
+  k_compact_fill<<<ceil_div(n, 256), 256, 0, st>>>(n, off0, T.m2l_off.get(), T.m2l_idx.get(), src.cell_cnt.get(),
+                                                    pos.get(), w->idx.get(), w->cell.get(), w->off.get());
+  FMM_CHECK_LAUNCH();
+  FMM_CUDA(cudaMemcpyAsync(w->off.get() + h[1], &h[0], sizeof(int), cudaMemcpyHostToDevice, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  c->m2l_cache.push_back(std::move(w));
+  return *c->m2l_cache.back();
+}
+
+void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
+  if (w.rows == 0) return;
+  const Tree& T = c->tree;
+#define FMM_ROT_CASE(PP)                                                                                       \
+  case PP:                                                                                                     \
+    k_m2l_rot<PP><<<w.rows, 32, 0, st>>>(w.cell.get(), w.off.get(), w.idx.get(), T.key.get(), c->Mx.get(),   \
+                                         c->Lx.get());                                                         \
+    break;
+  switch (c->P) {
+    FMM_ROT_CASE(8) FMM_ROT_CASE(10) FMM_ROT_CASE(12)
+    default: throw Error(FMMBEM_E_INVALID, "rotation M2L not instantiated for this P");
+  }
+#undef FMM_ROT_CASE
+  FMM_CHECK_LAUNCH();
+}
+
+}  // namespace fmm

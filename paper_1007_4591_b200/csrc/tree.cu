@@ -315,6 +315,8 @@ void bbox(const double* p, int64_t n, double mn[3], double mx[3], cudaStream_t s
 
 }  // namespace
 
+void scan_ints(const int* in, int* out, int n, cudaStream_t s) { exclusive_scan(in, out, n, s); }
+
 // Device-side inputs of the tree build (FP64, caller order).
 void build_tree(fmmbem_ctx* c, const double* cen, const double* nrm, const double* area, const double* qpts,
                 const double* wq, const double* cxyz, const double* cq, cudaStream_t s) {
