@@ -150,8 +150,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5")
-    ap.add_argument("--terms", type=int, default=10)
-    ap.add_argument("--leaf-points", type=int, default=64)
+    ap.add_argument("--terms", type=int, default=12)
+    ap.add_argument("--leaf-points", type=int, default=128)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--cpu-rows", type=int, default=128, help="oracle sample rows for cpu_baseline/parity")

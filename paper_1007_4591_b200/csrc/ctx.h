@@ -47,6 +47,13 @@ struct M2LWork {
   DevBuf<int> off;   // [rows + 1]
 };
 
+// P2P work items (leaf, first target, count) of one target set
+struct P2PItems {
+  const PointSet* tgt = nullptr;
+  int64_t n = 0;
+  DevBuf<int4> items;
+};
+
 struct Timing {
   cudaEvent_t ev[12];
   bool valid = false;
@@ -85,6 +92,7 @@ struct fmmbem_ctx {
   fmm::DevBuf<double> part; // partial sums [blocks * (m+2)]
 
   std::vector<std::unique_ptr<fmm::M2LWork>> m2l_cache;
+  std::vector<std::unique_ptr<fmm::P2PItems>> p2p_cache;
   int m2l_mode = 0;  // 0 = rotation O(P^3) when available, 1 = plain O(P^4)
   int64_t p2p_inter_kp = 0, p2p_inter_chg = 0;  // exact interaction counts
   int64_t m2l_pairs_kp = 0;

@@ -34,6 +34,7 @@ void build_tree(fmmbem_ctx* c, const double* cen, const double* nrm, const doubl
 // near field; writes y = ax x + b raw (overwrites)
 void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
                 bool direct, cudaStream_t st);
+const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t);
 // exact interaction count of launch_p2p(t, s) (list mode) -- setup-time helper
 int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct);
 

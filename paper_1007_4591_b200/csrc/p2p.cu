@@ -2,14 +2,16 @@
 // contribution is obtained from directly computing the interactions between all the points
 // in the adjacent cells", "P2P ... the largest fractions").
 //
-// One CTA per target leaf.  The sources of the (<= 27) neighbour leaves are streamed through
-// shared memory in tiles, already shifted into the target leaf's frame: offsets between
-// leaf centres are exact multiples of the leaf width (FP32-exact), so the
-// subtraction s - x involves two numbers of leaf size only.  Every warp reads one source per
-// step (broadcast LDS.128); threads own targets (no atomics, fixed summation order).  When a
-// leaf has fewer targets than threads, the sources are split between thread groups and the
-// partial sums reduced in shared memory (split-K).  The self-leaf block is the only masked
-// block (j != i of the discrete operator).
+// Work unit = one warp = one chunk of <= 32*T targets of one leaf (T targets per lane in
+// registers).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
+// and a tail chunk with few targets spreads its lanes over S source subsets (split-K, reduced in
+// shared memory) -- lanes stay busy whatever the occupancy.  The sources of the (<= 27)
+// neighbour leaves stream through a warp-private shared-memory tile, already shifted into the
+// target leaf's frame: offsets between leaf centres are exact multiples of the leaf width
+// (FP32-exact), so s - x subtracts two numbers of leaf size only.  All lanes of a
+// subset read the same source (broadcast LDS.128).  Outputs are owned by one lane (no atomics,
+// fixed summation order -> bitwise reproducible).  Only the self-leaf block is masked (j != i of
+// the discrete operator).
 //
 // Raw outputs, un-normalised potential phi = sum_j w_j / r_ij:
 //   pot = phi(x_i),   dn = n_i . grad phi(x_i) = n_i . sum_j w_j (y_j - x_i) / r^3
@@ -21,11 +23,11 @@ namespace fmm {
 
 namespace {
 
-constexpr int TPB = 128;
-constexpr int TILE = 1024;
+constexpr int TILE = 128;   // sources per warp tile
 constexpr int MAXSEG = 32;
 
 struct P2PArgs {
+  const int4* items;  // (leaf, first target, target count, 0)
   const float4* tpos;
   const float4* tnrm;
   const int* tbeg;
@@ -43,13 +45,6 @@ struct P2PArgs {
   OutArg pot, dn;
   int* flag;
 };
-
-__device__ __forceinline__ void load_src(const P2PArgs& a, int j, float sx, float sy, float sz, float4* dst) {
-  float4 p = __ldg(a.spos + j);
-  float w = p.w;
-  if (a.sx) w *= __ldg(a.sx + (a.sdiv == 1 ? j : j / a.sdiv));
-  *dst = make_float4(p.x + sx, p.y + sy, p.z + sz, w);
-}
 
 template <bool POT, bool DN, bool MASK, bool CHECK>
 __device__ __forceinline__ void interact(const float4 s, float px, float py, float pz, float& ap, float& gx,
@@ -75,59 +70,51 @@ __device__ __forceinline__ void interact(const float4 s, float px, float py, flo
   }
 }
 
-template <bool POT, bool DN, bool SELF, bool CHECK>
-__global__ void __launch_bounds__(TPB) k_p2p(P2PArgs a) {
+template <int T, bool POT, bool DN, bool SELF, bool CHECK>
+__global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   __shared__ float4 tile[TILE];
   __shared__ int own[SELF ? TILE : 1];
   __shared__ int seg_src[MAXSEG], seg_cum[MAXSEG + 1];
   __shared__ float4 seg_sh[MAXSEG];
-  __shared__ float red[4][TPB];
-  __shared__ int s_nseg;
+  __shared__ float red[4 * T][32];
 
-  const int leaf = blockIdx.x;
-  const int tb = a.tbeg[leaf];
-  const int nt = a.tbeg[leaf + 1] - tb;
-  if (nt == 0) return;
+  const int4 it = a.items[blockIdx.x];
+  const int leaf = it.x, tb = it.y, nt = it.z;
+  const int lane = threadIdx.x;
   const int4 tc = a.ijk[leaf];
-  const int tid = threadIdx.x;
 
   // ---- source segments: neighbour leaves (self last) or, in direct mode, everything
-  int n_src, self_lo, self_hi;  // self block = virtual range [self_lo, self_hi)
+  int n_src, self_lo, self_hi, nseg = 0;
   if (!a.direct) {
-    if (tid < 32) {
-      const int o = a.nbr_off[leaf], nn = a.nbr_off[leaf + 1] - o;
-      int s = -1, cnt = 0, beg = 0;
-      bool valid = tid < nn;
-      if (valid) {
-        s = a.nbr_idx[o + tid];
-        beg = a.sbeg[s];
-        cnt = a.sbeg[s + 1] - beg;
-      }
-      bool is_self = valid && s == leaf;
-      unsigned vmask = __ballot_sync(0xffffffffu, valid && !is_self);
-      int rank = is_self ? __popc(vmask) : __popc(vmask & ((1u << tid) - 1));
-      if (valid) {
-        seg_src[rank] = beg;
-        int4 sc = a.ijk[s];
-        seg_sh[rank] = make_float4((sc.x - tc.x) * a.h, (sc.y - tc.y) * a.h, (sc.z - tc.z) * a.h, 0.f);
-      }
-      if (valid) seg_cum[rank + 1] = cnt;  // counts in rank order (scanned below)
-      __syncwarp();
-      int my_cnt = (tid < nn) ? seg_cum[tid + 1] : 0;
-      __syncwarp();
-      int incl = my_cnt;
-      for (int d = 1; d < 32; d <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, d);
-        if (tid >= d) incl += v;
-      }
-      if (tid < nn) seg_cum[tid + 1] = incl;
-      if (tid == 0) {
-        seg_cum[0] = 0;
-        s_nseg = nn;
-      }
+    const int o = a.nbr_off[leaf], nn = a.nbr_off[leaf + 1] - o;
+    int s = -1, cnt = 0, beg = 0;
+    const bool valid = lane < nn;
+    if (valid) {
+      s = a.nbr_idx[o + lane];
+      beg = a.sbeg[s];
+      cnt = a.sbeg[s + 1] - beg;
     }
-    __syncthreads();
-    const int nn = s_nseg;
+    const bool is_self = valid && s == leaf;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid && !is_self);
+    const int rank = is_self ? __popc(vmask) : __popc(vmask & ((1u << lane) - 1));
+    if (valid) {
+      seg_src[rank] = beg;
+      int4 sc = a.ijk[s];
+      seg_sh[rank] = make_float4((sc.x - tc.x) * a.h, (sc.y - tc.y) * a.h, (sc.z - tc.z) * a.h, 0.f);
+      seg_cum[rank + 1] = cnt;
+    }
+    __syncwarp();
+    int incl = (lane < nn) ? seg_cum[lane + 1] : 0;
+    __syncwarp();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (lane < nn) seg_cum[lane + 1] = incl;
+    if (lane == 0) seg_cum[0] = 0;
+    __syncwarp();
+    nseg = nn;
     n_src = seg_cum[nn];
     if (SELF) {
       self_lo = seg_cum[nn - 1];
@@ -141,84 +128,121 @@ __global__ void __launch_bounds__(TPB) k_p2p(P2PArgs a) {
     self_hi = a.sbeg[leaf + 1];
   }
 
-  const int tch = nt <= 32 ? 32 : (nt <= 64 ? 64 : 128);
-  const int split = TPB / tch;
-  const int lt = tid % tch, grp = tid / tch;
+  // ---- lane mapping: tl-th target slot, source subset sub of S
+  const int nl_t = (nt + T - 1) / T;          // lanes needed per subset (<= 32)
+  const int S = 32 / nl_t;                    // source subsets
+  const int tl = lane % nl_t, sub = lane / nl_t;
+  const bool lvalid = sub < S;
+  int ti[T];
+  float4 tp[T];
+  float ap[T], gx[T], gy[T], gz[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const int il = tl + k * nl_t;
+    ti[k] = tb + (il < nt ? il : 0);
+    tp[k] = a.tpos[ti[k]];
+    ap[k] = gx[k] = gy[k] = gz[k] = 0.f;
+  }
+  const int step = lvalid ? S : 0;
 
-  for (int t0 = 0; t0 < nt; t0 += tch) {
-    const int il = t0 + lt;
-    const bool tvalid = il < nt;
-    const int i = tb + (tvalid ? il : 0);
-    float4 tp = a.tpos[i];
-    float ap = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
-
-    for (int base = 0; base < n_src; base += TILE) {
-      const int tcnt = min(TILE, n_src - base);
-      __syncthreads();
-      for (int k = tid; k < tcnt; k += TPB) {
+  for (int base = 0; base < n_src; base += TILE) {
+    const int tcnt = min(TILE, n_src - base);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < TILE / 32; ++q) {
+      const int k = lane + 32 * q;
+      if (k < tcnt) {
         const int v = base + k;
         int j;
         float sx, sy, sz;
         if (!a.direct) {
-          int lo = 0, hi = s_nseg - 1;  // last segment with seg_cum[seg] <= v
+          int lo = 0, hi = nseg - 1;  // last segment with seg_cum[seg] <= v
           while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
             if (seg_cum[mid] <= v) lo = mid; else hi = mid - 1;
           }
           j = seg_src[lo] + (v - seg_cum[lo]);
-          float4 sh = seg_sh[lo];
+          const float4 sh = seg_sh[lo];
           sx = sh.x; sy = sh.y; sz = sh.z;
         } else {
           j = v;
-          int4 sc = a.ijk[a.sleaf[j]];
+          const int4 sc = a.ijk[a.sleaf[j]];
           sx = (sc.x - tc.x) * a.h; sy = (sc.y - tc.y) * a.h; sz = (sc.z - tc.z) * a.h;
         }
-        load_src(a, j, sx, sy, sz, &tile[k]);
+        const float4 p = __ldg(a.spos + j);
+        float w = p.w;
+        if (a.sx) w *= __ldg(a.sx + (a.sdiv == 1 ? j : j / a.sdiv));
+        tile[k] = make_float4(p.x + sx, p.y + sy, p.z + sz, w);
         if (SELF) own[k] = (a.sdiv == 1) ? j : j / a.sdiv;
       }
-      __syncthreads();
-      // unmasked range of this tile: [0, tcnt) minus the self block
-      int mlo = SELF ? min(max(self_lo - base, 0), tcnt) : tcnt;
-      int mhi = SELF ? min(max(self_hi - base, 0), tcnt) : tcnt;
-      // part 1: [0, mlo) and [mhi, tcnt) unmasked
-#pragma unroll 4
-      for (int k = grp; k < mlo; k += split)
-        interact<POT, DN, false, CHECK>(tile[k], tp.x, tp.y, tp.z, ap, gx, gy, gz, false, a.flag);
-      if (SELF) {
-        int k0 = mhi + ((grp - mhi) % split + split) % split;
-#pragma unroll 4
-        for (int k = k0; k < tcnt; k += split)
-          interact<POT, DN, false, CHECK>(tile[k], tp.x, tp.y, tp.z, ap, gx, gy, gz, false, a.flag);
-        int k1 = mlo + ((grp - mlo) % split + split) % split;
-        for (int k = k1; k < mhi; k += split)
-          interact<POT, DN, true, CHECK>(tile[k], tp.x, tp.y, tp.z, ap, gx, gy, gz, own[k] == i, a.flag);
+    }
+    __syncwarp();
+    if (!lvalid) continue;
+    const int mlo = SELF ? min(max(self_lo - base, 0), tcnt) : tcnt;
+    const int mhi = SELF ? min(max(self_hi - base, 0), tcnt) : tcnt;
+    // unmasked: [0, mlo) and [mhi, tcnt)
+#pragma unroll 2
+    for (int k = sub; k < mlo; k += step) {
+      const float4 s = tile[k];
+#pragma unroll
+      for (int q = 0; q < T; ++q)
+        interact<POT, DN, false, CHECK>(s, tp[q].x, tp[q].y, tp[q].z, ap[q], gx[q], gy[q], gz[q], false, a.flag);
+    }
+    if (SELF) {
+      int k0 = mhi + ((sub - mhi) % S + S) % S;
+#pragma unroll 2
+      for (int k = k0; k < tcnt; k += step) {
+        const float4 s = tile[k];
+#pragma unroll
+        for (int q = 0; q < T; ++q)
+          interact<POT, DN, false, CHECK>(s, tp[q].x, tp[q].y, tp[q].z, ap[q], gx[q], gy[q], gz[q], false, a.flag);
+      }
+      int k1 = mlo + ((sub - mlo) % S + S) % S;
+      for (int k = k1; k < mhi; k += step) {
+        const float4 s = tile[k];
+        const int o = own[k];
+#pragma unroll
+        for (int q = 0; q < T; ++q)
+          interact<POT, DN, true, CHECK>(s, tp[q].x, tp[q].y, tp[q].z, ap[q], gx[q], gy[q], gz[q], o == ti[q],
+                                         a.flag);
       }
     }
-    // split-K reduction
-    if (split > 1) {
-      red[0][tid] = ap;
-      red[1][tid] = gx;
-      red[2][tid] = gy;
-      red[3][tid] = gz;
-      __syncthreads();
-      if (grp == 0) {
-        for (int g = 1; g < split; ++g) {
-          ap += red[0][g * tch + lt];
-          gx += red[1][g * tch + lt];
-          gy += red[2][g * tch + lt];
-          gz += red[3][g * tch + lt];
+  }
+  // ---- split-K reduction over the S subsets
+  if (S > 1) {
+#pragma unroll
+    for (int q = 0; q < T; ++q) {
+      red[4 * q + 0][lane] = ap[q];
+      red[4 * q + 1][lane] = gx[q];
+      red[4 * q + 2][lane] = gy[q];
+      red[4 * q + 3][lane] = gz[q];
+    }
+    __syncwarp();
+    if (sub == 0) {
+      for (int g = 1; g < S; ++g) {
+#pragma unroll
+        for (int q = 0; q < T; ++q) {
+          ap[q] += red[4 * q + 0][g * nl_t + tl];
+          gx[q] += red[4 * q + 1][g * nl_t + tl];
+          gy[q] += red[4 * q + 2][g * nl_t + tl];
+          gz[q] += red[4 * q + 3][g * nl_t + tl];
         }
       }
     }
-    if (grp == 0 && tvalid) {
+  }
+  if (sub == 0) {
+#pragma unroll
+    for (int q = 0; q < T; ++q) {
+      if (tl + q * nl_t >= nt) continue;
+      const int i = ti[q];
       if (POT) {
-        float v = a.pot.b * ap;
+        float v = a.pot.b * ap[q];
         if (a.pot.x) v = fmaf(a.pot.ax, a.pot.x[i], v);
         a.pot.y[i] = v;
       }
       if (DN) {
-        float4 n = a.tnrm[i];
-        float v = a.dn.b * fmaf(n.x, gx, fmaf(n.y, gy, n.z * gz));
+        const float4 n = a.tnrm[i];
+        float v = a.dn.b * fmaf(n.x, gx[q], fmaf(n.y, gy[q], n.z * gz[q]));
         if (a.dn.x) v = fmaf(a.dn.ax, a.dn.x[i], v);
         a.dn.y[i] = v;
       }
@@ -226,15 +250,17 @@ __global__ void __launch_bounds__(TPB) k_p2p(P2PArgs a) {
   }
 }
 
+constexpr int P2P_T = 2;  // targets per lane
+
 template <bool SELF, bool CHECK>
 void dispatch(const P2PArgs& a, bool pot, bool dn, int grid, cudaStream_t st) {
-  if (pot && dn) k_p2p<true, true, SELF, CHECK><<<grid, TPB, 0, st>>>(a);
-  else if (pot) k_p2p<true, false, SELF, CHECK><<<grid, TPB, 0, st>>>(a);
-  else k_p2p<false, true, SELF, CHECK><<<grid, TPB, 0, st>>>(a);
+  if (pot && dn) k_p2p<P2P_T, true, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+  else if (pot) k_p2p<P2P_T, true, false, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+  else k_p2p<P2P_T, false, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
 }
 
 __global__ void k_count(int nl, const int* __restrict__ tbeg, const int* __restrict__ sbeg,
-                        const int* __restrict__ off, const int* __restrict__ idx, int direct, int ns, int self,
+                        const int* __restrict__ off, const int* __restrict__ idx, int direct, int ns,
                         unsigned long long* out) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long c = 0;
@@ -250,12 +276,59 @@ __global__ void k_count(int nl, const int* __restrict__ tbeg, const int* __restr
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+__global__ void k_item_count(int nl, const int* __restrict__ tbeg, int chunk, int* cnt) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nl) cnt[k] = (tbeg[k + 1] - tbeg[k] + chunk - 1) / chunk;
+}
+
+__global__ void k_item_fill(int nl, const int* __restrict__ tbeg, int chunk, const int* __restrict__ pos,
+                            int4* items) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nl) return;
+  const int b = tbeg[k], e = tbeg[k + 1];
+  int w = pos[k];
+  for (int t = b; t < e; t += chunk) items[w++] = make_int4(k, t, min(chunk, e - t), 0);
+}
+
 }  // namespace
+
+// (leaf, target chunk) work items of one target set, built once and cached
+const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t) {
+  for (auto& w : c->p2p_cache)
+    if (w->tgt == &t) return *w;
+  const int nl = (int)c->tree.n_leaves;
+  const int chunk = 32 * P2P_T;
+  cudaStream_t st = c->stream;
+  auto w = std::make_unique<P2PItems>();
+  w->tgt = &t;
+  DevBuf<int> cnt, pos;
+  cnt.alloc(nl + 1);
+  pos.alloc(nl + 1);
+  cnt.zero(st);
+  k_item_count<<<ceil_div(nl, 256), 256, 0, st>>>(nl, t.begin.get(), chunk, cnt.get());
+  FMM_CHECK_LAUNCH();
+  scan_ints(cnt.get(), pos.get(), nl + 1, st);
+  int n = 0;
+  FMM_CUDA(cudaMemcpyAsync(&n, pos.get() + nl, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  w->n = n;
+  w->items.alloc(std::max(1, n));
+  k_item_fill<<<ceil_div(nl, 256), 256, 0, st>>>(nl, t.begin.get(), chunk, pos.get(), w->items.get());
+  FMM_CHECK_LAUNCH();
+  FMM_CUDA(cudaStreamSynchronize(st));
+  c->p2p_cache.push_back(std::move(w));
+  return *c->p2p_cache.back();
+}
 
 void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
                 bool direct, cudaStream_t st) {
   const Tree& T = c->tree;
+  const bool pot = o.pot.y != nullptr, dn = o.dn.y != nullptr;
+  if (!pot && !dn) return;
+  const P2PItems& items = p2p_items(c, *t.set);
+  if (items.n == 0) return;
   P2PArgs a{};
+  a.items = items.items.get();
   a.tpos = t.set->pos.get();
   a.tnrm = t.set->nrm.get();
   a.tbeg = t.set->begin.get();
@@ -273,11 +346,8 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   a.pot = o.pot;
   a.dn = o.dn;
   a.flag = c->flag.get();
-  const bool pot = o.pot.y != nullptr, dn = o.dn.y != nullptr;
-  if (!pot && !dn) return;
   if (dn && !a.tnrm) throw Error(FMMBEM_E_INVALID, "normal derivative requested at targets without normals");
-  const int grid = (int)T.n_leaves;
-  if (grid == 0) return;
+  const int grid = (int)items.n;
   if (self) {
     if (check) dispatch<true, true>(a, pot, dn, grid, st);
     else dispatch<true, false>(a, pot, dn, grid, st);
@@ -295,7 +365,7 @@ int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self
   out.zero(c->stream);
   int nl = (int)T.n_leaves;
   k_count<<<ceil_div(nl, 256), 256, 0, c->stream>>>(nl, t.begin.get(), s.begin.get(), T.nbr_off.get(),
-                                                     T.nbr_idx.get(), direct ? 1 : 0, (int)s.n, self, out.get());
+                                                     T.nbr_idx.get(), direct ? 1 : 0, (int)s.n, out.get());
   FMM_CHECK_LAUNCH();
   unsigned long long h = 0;
   FMM_CUDA(cudaMemcpyAsync(&h, out.get(), sizeof(h), cudaMemcpyDeviceToHost, c->stream));
