@@ -120,11 +120,13 @@ __global__ void __launch_bounds__(128) k_p2m(const float4* __restrict__ pos, con
 __global__ void __launch_bounds__(64) k_m2m(int lvl_off, int P, const int* __restrict__ cb,
                                             const int* __restrict__ ce, const uint64_t* __restrict__ key,
                                             const int* __restrict__ scnt, float2* __restrict__ M) {
-  extern __shared__ float2 smc[];  // [8][NC]
+  extern __shared__ float2 smc[];  // [8][NC] children, then [8][NC] R(d_octant)
   __shared__ int oct[8];
   const int cell = lvl_off + blockIdx.x;
   const int NC = P * (P + 1) / 2;
   if (scnt[cell] == 0) return;
+  float2* sR = smc + 8 * NC;
+  for (int t = threadIdx.x; t < 8 * NC; t += blockDim.x) sR[t] = c_R8[t / NC][t % NC];
   const int c0 = cb[cell], nch = ce[cell] - c0;
   for (int t = threadIdx.x; t < nch * NC; t += blockDim.x) {
     int ch = t / NC, c = t - ch * NC;
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(64) k_m2m(int lvl_off, int P, const int* __res
     float2 acc = make_float2(0.f, 0.f);
     for (int ch = 0; ch < nch; ++ch) {
       const float2* Mc = smc + ch * NC;
-      const float2* R = c_R8[oct[ch]];
+      const float2* R = sR + oct[ch] * NC;
       float sc = 1.f;
       for (int j = 0; j <= n; ++j, sc *= 0.5f) {
         const int nj = n - j;
@@ -248,14 +250,18 @@ __global__ void __launch_bounds__(M2L_TPB) k_m2l(int cell_off, int P, const int*
 __global__ void __launch_bounds__(64) k_l2l(int lvl_off, int P, const int* __restrict__ parent,
                                             const uint64_t* __restrict__ key, const int* __restrict__ tcnt,
                                             float2* __restrict__ Lx) {
-  extern __shared__ float2 sp[];  // parent L~ [NC]
+  extern __shared__ float2 sp[];  // parent L~ [NC], then R(d_octant) [NC]
   const int cell = lvl_off + blockIdx.x;
   if (tcnt[cell] == 0) return;
   const int NC = P * (P + 1) / 2;
   const int p = parent[cell];
-  for (int t = threadIdx.x; t < NC; t += blockDim.x) sp[t] = Lx[(size_t)p * NC + t];
+  const int oc = (int)(key[cell] & 7);
+  float2* R = sp + NC;
+  for (int t = threadIdx.x; t < NC; t += blockDim.x) {
+    sp[t] = Lx[(size_t)p * NC + t];
+    R[t] = c_R8[oc][t];
+  }
   __syncthreads();
-  const float2* R = c_R8[key[cell] & 7];
   for (int c = threadIdx.x; c < NC; c += blockDim.x) {
     int j = 0;
     while ((j + 1) * (j + 2) / 2 <= c) ++j;
@@ -419,12 +425,17 @@ void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
   if (L < 2) return;
   c->Mx.zero(st);
   const PointSet& S = *s.set;
-  k_p2m<<<(int)T.n_leaves, 128, 0, st>>>(S.pos.get(), s.x, S.div, S.begin.get(), P, (float)(1.0 / T.width(L)),
-                                         (int)T.lvl_off[L], c->Mx.get());
-  FMM_CHECK_LAUNCH();
+  if (exp_specialised(P)) {
+    launch_p2m_t(P, (int)T.n_leaves, S.pos.get(), s.x, S.div, S.begin.get(), (float)(1.0 / T.width(L)),
+                 (int)T.lvl_off[L], c->Mx.get(), st);
+  } else {
+    k_p2m<<<(int)T.n_leaves, 128, 0, st>>>(S.pos.get(), s.x, S.div, S.begin.get(), P, (float)(1.0 / T.width(L)),
+                                           (int)T.lvl_off[L], c->Mx.get());
+    FMM_CHECK_LAUNCH();
+  }
   for (int l = L - 1; l >= 2; --l) {
     int n = (int)(T.lvl_off[l + 1] - T.lvl_off[l]);
-    k_m2m<<<n, 64, 8 * NC * sizeof(float2), st>>>((int)T.lvl_off[l], P, T.child_begin.get(), T.child_end.get(),
+    k_m2m<<<n, 64, 16 * NC * sizeof(float2), st>>>((int)T.lvl_off[l], P, T.child_begin.get(), T.child_end.get(),
                                                    T.key.get(), S.cell_cnt.get(), c->Mx.get());
     FMM_CHECK_LAUNCH();
   }
@@ -458,7 +469,7 @@ void launch_downward(fmmbem_ctx* c, const PointSet& tgt, cudaStream_t st) {
   if (L < 2) return;
   for (int l = 2; l < L; ++l) {
     int n = (int)(T.lvl_off[l + 2] - T.lvl_off[l + 1]);
-    k_l2l<<<n, 64, NC * sizeof(float2), st>>>((int)T.lvl_off[l + 1], P, T.parent.get(), T.key.get(),
+    k_l2l<<<n, 64, 2 * NC * sizeof(float2), st>>>((int)T.lvl_off[l + 1], P, T.parent.get(), T.key.get(),
                                               tgt.cell_cnt.get(), c->Lx.get());
     FMM_CHECK_LAUNCH();
   }
@@ -469,6 +480,11 @@ void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t s
   const int L = T.L;
   if (L < 2) return;
   const PointSet& S = *t.set;
+  if (exp_specialised(c->P)) {
+    launch_l2p_t(c->P, (int)T.n_leaves, S.pos.get(), S.nrm.get(), S.begin.get(), (float)(1.0 / T.width(L)),
+                 (int)T.lvl_off[L], c->Lx.get(), o.pot, o.dn, st);
+    return;
+  }
   k_l2p<<<(int)T.n_leaves, 128, 0, st>>>(S.pos.get(), S.nrm.get(), S.begin.get(), c->P, (float)(1.0 / T.width(L)),
                                          (int)T.lvl_off[L], c->Lx.get(), o.pot, o.dn);
   FMM_CHECK_LAUNCH();

@@ -45,6 +45,13 @@ void launch_downward(fmmbem_ctx* c, const PointSet& tgt, cudaStream_t st);
 void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t st);
 void init_tables(fmmbem_ctx* c);
 
+// order-specialised P2M / L2P (expansions.cu)
+bool exp_specialised(int P);
+void launch_p2m_t(int P, int grid, const float4* pos, const float* x, int div, const int* beg, float inv_w,
+                  int leaf_off, float2* M, cudaStream_t st);
+void launch_l2p_t(int P, int grid, const float4* pos, const float4* nrm, const int* beg, float inv_w, int leaf_off,
+                  const float2* Lx, const OutArg& pot, const OutArg& dn, cudaStream_t st);
+
 // rotation-accelerated M2L (m2l_rot.cu)
 bool rot_supported(int P);
 void init_rot_tables();
