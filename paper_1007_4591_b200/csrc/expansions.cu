@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, co
   float* slot = sv + lane;
 #pragma unroll
   for (int m = 0; m < P; ++m) {
-    float ar[P - m], ai[P - m];
+    float ar[P], ai[P];
 #pragma unroll
     for (int k = 0; k < P - m; ++k) ar[k] = ai[k] = 0.f;
     for (int j = b + lane; j < e; j += 32) {
