@@ -16,6 +16,51 @@ namespace {
 
 __host__ __device__ constexpr int cx(int n, int m) { return n * (n + 1) / 2 + m; }
 
+// one order column m of the P2M sums of this lane's sources into the lane's slot
+template <int P, int m>
+__device__ __forceinline__ void p2m_column(float* slot, const float4* __restrict__ pos, const float* __restrict__ x,
+                                           int div, int b, int e, int lane, float inv_w) {
+  float ar[P - m], ai[P - m];
+#pragma unroll
+  for (int k = 0; k < P - m; ++k) ar[k] = ai[k] = 0.f;
+  for (int j = b + lane; j < e; j += 32) {
+    const float4 p = __ldg(pos + j);
+    float w = p.w;
+    if (x) w *= __ldg(x + (div == 1 ? j : j / div));
+    const float ux = p.x * inv_w, uy = p.y * inv_w, uz = p.z * inv_w;
+    const float r2 = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
+    float rr = 1.f, ri = 0.f;  // R_m^m = (-(x + i y)/2)^m / m!
+#pragma unroll
+    for (int k = 1; k <= m; ++k) {
+      const float s = -0.5f / (float)k;
+      const float t = (rr * ux - ri * uy) * s;
+      ri = (rr * uy + ri * ux) * s;
+      rr = t;
+    }
+    float pr = 0.f, pi = 0.f, cr = rr, ci = ri;
+    ar[0] = fmaf(w, cr, ar[0]);
+    ai[0] = fmaf(-w, ci, ai[0]);
+#pragma unroll
+    for (int n = m + 1; n < P; ++n) {
+      const float inv = 1.f / (float)((n - m) * (n + m));
+      const float a = (float)(2 * n - 1) * inv * uz, bb = r2 * inv;
+      const float nr = a * cr - bb * pr, ni = a * ci - bb * pi;
+      pr = cr;
+      pi = ci;
+      cr = nr;
+      ci = ni;
+      ar[n - m] = fmaf(w, cr, ar[n - m]);
+      ai[n - m] = fmaf(-w, ci, ai[n - m]);
+    }
+  }
+#pragma unroll
+  for (int n = m; n < P; ++n) {
+    slot[(2 * cx(n, m)) * 33] = ar[n - m];
+    slot[(2 * cx(n, m) + 1) * 33] = ai[n - m];
+  }
+  if constexpr (m + 1 < P) p2m_column<P, m + 1>(slot, pos, x, div, b, e, lane, inv_w);
+}
+
 template <int P>
 __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
                                               const int* __restrict__ beg, float inv_w, int leaf_off,
@@ -26,48 +71,7 @@ __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, co
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
-  float* slot = sv + lane;
-#pragma unroll
-  for (int m = 0; m < P; ++m) {
-    float ar[P], ai[P];
-#pragma unroll
-    for (int k = 0; k < P - m; ++k) ar[k] = ai[k] = 0.f;
-    for (int j = b + lane; j < e; j += 32) {
-      const float4 p = __ldg(pos + j);
-      float w = p.w;
-      if (x) w *= __ldg(x + (div == 1 ? j : j / div));
-      const float ux = p.x * inv_w, uy = p.y * inv_w, uz = p.z * inv_w;
-      const float r2 = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-      float rr = 1.f, ri = 0.f;  // R_m^m = (-(x + i y)/2)^m / m!
-#pragma unroll
-      for (int k = 1; k <= m; ++k) {
-        const float s = -0.5f / (float)k;
-        const float t = (rr * ux - ri * uy) * s;
-        ri = (rr * uy + ri * ux) * s;
-        rr = t;
-      }
-      float pr = 0.f, pi = 0.f, cr = rr, ci = ri;
-      ar[0] = fmaf(w, cr, ar[0]);
-      ai[0] = fmaf(-w, ci, ai[0]);
-#pragma unroll
-      for (int n = m + 1; n < P; ++n) {
-        const float inv = 1.f / (float)((n - m) * (n + m));
-        const float a = (float)(2 * n - 1) * inv * uz, bb = r2 * inv;
-        const float nr = a * cr - bb * pr, ni = a * ci - bb * pi;
-        pr = cr;
-        pi = ci;
-        cr = nr;
-        ci = ni;
-        ar[n - m] = fmaf(w, cr, ar[n - m]);
-        ai[n - m] = fmaf(-w, ci, ai[n - m]);
-      }
-    }
-#pragma unroll
-    for (int n = m; n < P; ++n) {
-      slot[(2 * cx(n, m)) * 33] = ar[n - m];
-      slot[(2 * cx(n, m) + 1) * 33] = ai[n - m];
-    }
-  }
+  p2m_column<P, 0>(sv + lane, pos, x, div, b, e, lane, inv_w);
   __syncwarp();
   for (int c = lane; c < NC; c += 32) {
     float sx = 0.f, sy = 0.f;
