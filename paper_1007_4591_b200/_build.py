@@ -17,7 +17,7 @@ INC = os.path.join(os.path.dirname(HERE), "include")
 OBJ = os.path.join(os.path.dirname(HERE), "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+NVCC_FLAGS = ["-O3", "-std=c++17", "-ftz=true", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
 
 
@@ -45,6 +45,11 @@ def build(force: bool = False, verbose: bool = True, extra=()) -> str:
     if not force and not needs_build():
         return LIB
     os.makedirs(OBJ, exist_ok=True)
+    stamp = os.path.join(OBJ, "flags.txt")
+    flags = " ".join([NVCC, *NVCC_FLAGS, *extra])
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
+        open(stamp, "w").write(flags)
     hdr_t = max(os.path.getmtime(f) for f in headers())
 
     def compile_one(src):

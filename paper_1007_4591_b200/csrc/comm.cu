@@ -1,0 +1,108 @@
+// comm.cu -- NCCL over NVLink/NVSwitch for the multi-GPU path (PAPER.md P:572-574:
+// "the partitioning of the tree among MPI processes ... the communication of needed data to
+// perform the FMM interactions", one process per GPU).
+//
+// libnccl is resolved at run time (dlopen of libnccl.so.2, i.e. the copy PyTorch already loaded
+// when present), so the library has no link-time NCCL dependency and single-GPU use never touches
+// it.  Only the handful of collectives the path needs are wrapped.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace fmm {
+
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi& api() {
+  static NcclApi a;
+  if (a.h) return a;
+  for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+    a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+    if (a.h) break;
+  }
+  if (!a.h) throw Error(FMMBEM_E_NCCL, "cannot dlopen libnccl.so.2");
+  auto sym = [&](const char* s) {
+    void* p = dlsym(a.h, s);
+    if (!p) throw Error(FMMBEM_E_NCCL, std::string("libnccl lacks ") + s);
+    return p;
+  };
+  a.getUniqueId = (decltype(a.getUniqueId))sym("ncclGetUniqueId");
+  a.commInitRank = (decltype(a.commInitRank))sym("ncclCommInitRank");
+  a.commDestroy = (decltype(a.commDestroy))sym("ncclCommDestroy");
+  a.allReduce = (decltype(a.allReduce))sym("ncclAllReduce");
+  a.broadcast = (decltype(a.broadcast))sym("ncclBroadcast");
+  a.groupStart = (decltype(a.groupStart))sym("ncclGroupStart");
+  a.groupEnd = (decltype(a.groupEnd))sym("ncclGroupEnd");
+  a.errStr = (decltype(a.errStr))sym("ncclGetErrorString");
+  return a;
+}
+
+void check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(FMMBEM_E_NCCL, std::string(what) + ": " + api().errStr(r));
+}
+
+}  // namespace
+
+void comm_unique_id(void* id128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  check(api().getUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(id128, &id, sizeof(id));
+}
+
+void comm_init(fmmbem_ctx* c, const void* id128) {
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t comm;
+  check(api().commInitRank(&comm, c->opt.nranks, id, c->opt.rank), "ncclCommInitRank");
+  c->comm = comm;
+}
+
+void comm_destroy(fmmbem_ctx* c) {
+  if (c->comm) api().commDestroy((ncclComm_t)c->comm);
+  c->comm = nullptr;
+}
+
+void comm_allreduce_f32(fmmbem_ctx* c, float* buf, size_t n, cudaStream_t s) {
+  if (c->opt.nranks <= 1 || n == 0) return;
+  check(api().allReduce(buf, buf, n, ncclFloat32, ncclSum, (ncclComm_t)c->comm, s), "ncclAllReduce");
+}
+
+void comm_allreduce_f64(fmmbem_ctx* c, double* buf, size_t n, cudaStream_t s) {
+  if (c->opt.nranks <= 1 || n == 0) return;
+  check(api().allReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)c->comm, s), "ncclAllReduce");
+}
+
+// full[offs[r] : offs[r+1]] <- rank r's slice, for every r (uneven slices: grouped broadcasts)
+void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const std::vector<int64_t>& offs,
+                         cudaStream_t s) {
+  const int R = c->opt.nranks;
+  check(api().groupStart(), "ncclGroupStart");
+  for (int r = 0; r < R; ++r) {
+    const size_t n = (size_t)(offs[r + 1] - offs[r]);
+    if (!n) continue;
+    check(api().broadcast(r == c->opt.rank ? (const void*)mine : (const void*)(full + offs[r]), full + offs[r], n,
+                          ncclFloat32, r, (ncclComm_t)c->comm, s),
+          "ncclBroadcast");
+  }
+  check(api().groupEnd(), "ncclGroupEnd");
+}
+
+}  // namespace fmm

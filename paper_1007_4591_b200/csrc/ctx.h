@@ -96,6 +96,7 @@ struct fmmbem_ctx {
   int m2l_mode = 0;  // 0 = rotation O(P^3) when available, 1 = plain O(P^4)
   int64_t p2p_inter_kp = 0, p2p_inter_chg = 0;  // exact interaction counts
   int64_t m2l_pairs_kp = 0;
+  void* comm = nullptr;  // ncclComm_t (nranks > 1)
   fmmbem_timing last{};
   cudaEvent_t ev[10] = {};
 };

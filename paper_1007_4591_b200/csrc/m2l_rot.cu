@@ -21,6 +21,7 @@
 // block (rotations) or one order column (coaxial translation) at a time, so registers stay low for
 // any P.  The 32 pairs of a warp belong to one target cell and are summed through the same slots.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.cuh"
@@ -148,16 +149,21 @@ __device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], co
   if constexpr (n + 1 < P) pass_c<P, n + 1>(sl, zar, zai, zbr, zbi, scale * irho, irho);
 }
 
-template <int P>
-__global__ void __launch_bounds__(32) k_m2l_rot(const int* __restrict__ tcells, const int* __restrict__ off,
-                                                const int* __restrict__ idx, const uint64_t* __restrict__ key,
-                                                const float2* __restrict__ M, float2* __restrict__ Lx) {
+// one warp per target cell; W warps per CTA start in lockstep on the same (long, unrolled) code
+template <int P, int W>
+__global__ void __launch_bounds__(32 * W) k_m2l_rot(int rows, const int* __restrict__ tcells,
+                                                    const int* __restrict__ off, const int* __restrict__ idx,
+                                                    const uint64_t* __restrict__ key, const float2* __restrict__ M,
+                                                    float2* __restrict__ Lx) {
   constexpr int NC = P * (P + 1) / 2;
   constexpr int NR = (NC + 31) / 32;
-  __shared__ float sv[2 * NC * 33];
-  const int cell = tcells[blockIdx.x];
-  const int lo = off[blockIdx.x], hi = off[blockIdx.x + 1];
-  const int lane = threadIdx.x;
+  __shared__ float svall[W][2 * NC * 33];
+  const int row = blockIdx.x * W + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float* sv = svall[threadIdx.x >> 5];
+  const int cell = tcells[row];
+  const int lo = off[row], hi = off[row + 1];
+  const int lane = threadIdx.x & 31;
   const Slot sl{sv + lane};
   int tx, ty, tz;
   demorton(key[cell], tx, ty, tz);
@@ -373,10 +379,18 @@ const M2LWork& m2l_work(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt,
 void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
   if (w.rows == 0) return;
   const Tree& T = c->tree;
-#define FMM_ROT_CASE(PP)                                                                                       \
-  case PP:                                                                                                     \
-    k_m2l_rot<PP><<<w.rows, 32, 0, st>>>(w.cell.get(), w.off.get(), w.idx.get(), T.key.get(), c->Mx.get(),   \
-                                         c->Lx.get());                                                         \
+  static const int warps = [] {
+    const char* e = std::getenv("FMMBEM_M2L_WARPS");
+    return e ? std::atoi(e) : 1;
+  }();
+#define FMM_ROT_CASE(PP)                                                                                     \
+  case PP:                                                                                                   \
+    if (warps == 2)                                                                                          \
+      k_m2l_rot<PP, 2><<<ceil_div(w.rows, 2), 64, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(),          \
+                                                            w.idx.get(), T.key.get(), c->Mx.get(), c->Lx.get()); \
+    else                                                                                                     \
+      k_m2l_rot<PP, 1><<<(int)w.rows, 32, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(), w.idx.get(),     \
+                                                   T.key.get(), c->Mx.get(), c->Lx.get());                   \
     break;
   switch (c->P) {
     FMM_ROT_CASE(8) FMM_ROT_CASE(10) FMM_ROT_CASE(12)
