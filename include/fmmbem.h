@@ -72,12 +72,23 @@ typedef struct {
   int32_t direct;        /* 1 = bypass the FMM: all-pairs P2P (paper Fig. 11 "direct") */
   int32_t deterministic; /* reductions have a fixed order (no atomics on results); always true */
   int32_t device;        /* CUDA ordinal used by this ctx */
-  int32_t rank, nranks;  /* one process per GPU; nranks > 1 is reserved (returns E_INVALID) */
-  const void* nccl_id;   /* reserved for nranks > 1 */
+  int32_t rank, nranks;  /* one process per GPU; every rank passes the FULL mesh and charges */
+  const void* nccl_id;   /* nranks > 1: the 128-byte id from fmmbem_get_unique_id() on rank 0, broadcast by the caller */
 } fmmbem_options;
 
 /* Fill *out with the defaults above.  Returns FMMBEM_E_INVALID if out is NULL. */
 fmmbem_status fmmbem_default_options(fmmbem_options* out);
+
+/* Multi-GPU bootstrap: writes a 128-byte NCCL unique id into id128_out (host).
+ * Call on rank 0 only and broadcast the bytes (e.g. torch.distributed) before fmmbem_create.
+ * Returns FMMBEM_E_NCCL when libnccl.so.2 cannot be loaded. */
+fmmbem_status fmmbem_get_unique_id(void* id128_out);
+
+/* Domain decomposition helper (cost-weighted): split n items with non-negative
+ * host costs into `parts` contiguous ranges of nearly equal total cost.  bounds (host, parts+1
+ * entries) receives 0 = bounds[0] <= ... <= bounds[parts] = n.  Pure host code; the library uses
+ * it on the leaves' P2P + M2L costs so that every rank derives the same partition. */
+fmmbem_status fmmbem_split_costs(const double* costs, int64_t n, int32_t parts, int64_t* bounds);
 
 /* Build the solver for one molecule (setup): validates and
  * deep-copies the inputs, derives panels and quadrature points (FP64, P:368-378,
@@ -92,8 +103,9 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* panels, const fmmbem_charges* cha
 void fmmbem_destroy(fmmbem_ctx* ctx);
 
 /* Vectors passed to matvec/solve/bibee are in the library's LOCAL order (the octree's
- * Morton order).  fmmbem_local_panel_ids writes, for local index i, the caller's
- * triangle index (host int64 array of fmmbem_num_local_panels entries). */
+ * Morton order) and, with nranks > 1, hold only this rank's panels (a contiguous range of
+ * Morton-ordered leaves of equal estimated work).  fmmbem_local_panel_ids writes, for local
+ * index i, the caller's triangle index (host int64 array of fmmbem_num_local_panels entries). */
 int64_t fmmbem_num_local_panels(const fmmbem_ctx* ctx);
 fmmbem_status fmmbem_local_panel_ids(const fmmbem_ctx* ctx, int64_t* global_ids_out);
 
@@ -105,7 +117,9 @@ typedef enum {
 
 /* One FMM matrix-vector product.  x_dev, y_dev: caller-owned device
  * arrays of fmmbem_num_local_panels floats in local order; must not alias.  Stream-ordered:
- * returns after enqueueing on cuda_stream; y is valid when the stream completes. */
+ * returns after enqueueing on cuda_stream; y is valid when the stream completes.  With nranks > 1
+ * the call is collective (all ranks, same order): x slices are all-gathered and the partial
+ * multipoles of every rank's subtrees are all-reduced over NCCL. */
 fmmbem_status fmmbem_matvec(fmmbem_ctx* ctx, fmmbem_op op, const float* x_dev, float* y_dev,
                             void* cuda_stream);
 
@@ -154,7 +168,8 @@ fmmbem_status fmmbem_charge_fields(fmmbem_ctx* ctx, float* En_dev, float* psi_de
 fmmbem_status fmmbem_reaction_potential(fmmbem_ctx* ctx, const float* sigma_dev, double* phi_host);
 
 typedef struct {
-  double tree, upward, m2l, p2p, l2p, near, comm, gmres, total; /* ms, last call */
+  double tree, upward, m2l, p2p, l2p, near, comm, gmres, total; /* ms of the last matvec:
+                             upward = P2M + M2M, m2l = M2L, l2p = L2L + L2P, comm = NCCL exchanges, gmres = last solve */
   int64_t p2p_interactions; /* exact pair count of the last matvec's P2P */
   int64_t m2l_pairs;        /* M2L translations of the last matvec */
 } fmmbem_timing;

@@ -5,6 +5,6 @@ this package is its thin ctypes binding.  There is no CPU fallback: `Solver` rai
 library is missing.
 """
 from ._lib import load, FmmbemError  # noqa: F401
-from .api import Solver, default_options  # noqa: F401
+from .api import Solver, default_options, get_unique_id, split_costs  # noqa: F401
 
-__all__ = ["Solver", "default_options", "load", "FmmbemError"]
+__all__ = ["Solver", "default_options", "get_unique_id", "split_costs", "load", "FmmbemError"]

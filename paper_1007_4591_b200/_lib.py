@@ -60,6 +60,8 @@ class TreeInfo(C.Structure):
 # symbol -> (restype, argtypes); every entry point declared in include/fmmbem.h
 SIGNATURES = {
     "fmmbem_default_options": (C.c_int, [C.POINTER(Options)]),
+    "fmmbem_get_unique_id": (C.c_int, [C.c_void_p]),
+    "fmmbem_split_costs": (C.c_int, [C.POINTER(C.c_double), C.c_int64, C.c_int32, C.POINTER(C.c_int64)]),
     "fmmbem_create": (C.c_int, [C.POINTER(Mesh), C.POINTER(Charges), C.c_double, C.c_double,
                                 C.POINTER(Options), C.POINTER(C.c_void_p)]),
     "fmmbem_destroy": (None, [C.c_void_p]),

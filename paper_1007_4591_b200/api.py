@@ -20,6 +20,22 @@ def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
+def get_unique_id() -> bytes:
+    """128-byte NCCL unique id for a multi-GPU Solver (call on rank 0, broadcast the bytes)."""
+    buf = C.create_string_buffer(128)
+    L.check(L.load().fmmbem_get_unique_id(buf))
+    return buf.raw
+
+
+def split_costs(costs, parts):
+    """Contiguous equal-cost split used by the domain decomposition (pure host code)."""
+    c = np.ascontiguousarray(costs, np.float64)
+    b = np.empty(parts + 1, np.int64)
+    L.check(L.load().fmmbem_split_costs(c.ctypes.data_as(C.POINTER(C.c_double)), len(c), parts,
+                                        b.ctypes.data_as(C.POINTER(C.c_int64))))
+    return b
+
+
 def default_options(**kw):
     lib = L.load()
     o = L.Options()
@@ -45,8 +61,15 @@ class Solver:
         cq = np.ascontiguousarray(np.zeros(0) if charge_q is None else charge_q, np.float64).reshape(-1)
         if len(cx) != len(cq):
             raise ValueError("charge_xyz and charge_q differ in length")
+        nccl_id = options.pop("nccl_id", None)
         self.options = default_options(**options)
         self.device = int(self.options.device)
+        self._id_buf = None
+        if self.options.nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nranks > 1 needs the 128-byte nccl_id of rank 0")
+            self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
+            self.options.nccl_id = C.cast(self._id_buf, C.c_void_p)
         mesh = L.Mesh(len(v), _dp(v), len(t), t.ctypes.data_as(C.POINTER(C.c_int32)))
         chg = L.Charges(len(cq), _dp(cx) if len(cq) else None, _dp(cq) if len(cq) else None)
         h = C.c_void_p()
@@ -64,6 +87,17 @@ class Solver:
     def from_config(cls, cfg, **options):
         return cls(cfg["vertices"], cfg["triangles"], cfg["charge_xyz"], cfg["charge_q"], cfg["eps_in"],
                    cfg["eps_out"], **options)
+
+    @classmethod
+    def distributed(cls, cfg, group=None, **options):
+        """One rank of a multi-GPU solver; torch.distributed must be initialised.  Rank 0 draws the
+        NCCL id and torch.distributed broadcasts it; every rank passes the full problem."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [get_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        return cls.from_config(cfg, rank=rank, nranks=world, nccl_id=obj[0], **options)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -112,27 +112,91 @@ struct DevGuard {
   }
 };
 
-const SrcArg kp_src(fmmbem_ctx* c, const float* x) {
+// leaf cost for the partition: P2P interactions + M2L translations (~600 interaction-equivalents
+// each at P = 12) + per-point work
+__global__ void k_leaf_cost(int nl, int leaf_cell0, const int* __restrict__ tbeg, const int* __restrict__ off,
+                            const int* __restrict__ idx, const int* __restrict__ m2l_off, double* cost,
+                            long long* p2p) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nl) return;
+  long long nt = tbeg[k + 1] - tbeg[k], s = 0;
+  for (int e = off[k]; e < off[k + 1]; ++e) s += tbeg[idx[e] + 1] - tbeg[idx[e]];
+  const int cell = leaf_cell0 + k;
+  const double m2l = (double)(m2l_off[cell + 1] - m2l_off[cell]);
+  p2p[k] = nt * s;
+  cost[k] = (double)(nt * s) + (nt ? 600.0 * m2l : 0.0) + 50.0 * (double)nt;
+}
+
+__global__ void k_own_leaf_counts(int nl, const int* __restrict__ begin, int mult, int leaf_off, int lo, int hi,
+                                  int* cnt) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nl) cnt[leaf_off + k] = (k >= lo && k < hi) ? (begin[k + 1] - begin[k]) * mult : 0;
+}
+
+__global__ void k_up_counts2(int n, int off, const int* __restrict__ cb, const int* __restrict__ ce, int* cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = 0;
+  for (int c = cb[off + i]; c < ce[off + i]; ++c) s += cnt[c];
+  cnt[off + i] = s;
+}
+
+bool multi(const fmmbem_ctx* c) { return c->nranks > 1; }
+
+// Sources of the panel operators (K', V, A): x_local is this rank's slice; with nranks > 1 it is
+// all-gathered (P2P needs the neighbours' weights) and P2M runs on the owned leaves only.
+SrcArg kp_src(fmmbem_ctx* c, const float* x_local, cudaStream_t st, bool* distributed) {
   SrcArg s;
   s.set = (c->K == 1) ? &c->pan : &c->quad;
-  s.x = x;
+  s.x = x_local;
+  *distributed = false;
+  if (multi(c)) {
+    c->xfull.alloc(c->np);
+    comm_allgatherv_f32(c, x_local, c->xfull.get(), c->pan_offs, st);
+    s.x = c->xfull.get();
+    s.leaf_lo = c->leaf_lo;
+    s.leaf_hi = c->leaf_hi;
+    s.cnt = (c->K == 1) ? c->pan_own_cnt.get() : c->quad_own_cnt.get();
+    *distributed = true;
+  }
   return s;
+}
+
+// targets = this rank's panels (all panels on one GPU)
+TgtArg own_targets(fmmbem_ctx* c, bool quad) {
+  TgtArg t;
+  t.set = quad ? &c->quad : &c->pan;
+  if (multi(c)) {
+    t.leaf_lo = c->leaf_lo;
+    t.leaf_hi = c->leaf_hi;
+    t.cnt = quad ? c->quad_own_cnt.get() : c->pan_own_cnt.get();
+  }
+  return t;
 }
 
 }  // namespace
 
 void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
-              cudaStream_t st, bool timing) {
+              cudaStream_t st, bool timing, bool distributed) {
   const bool direct = c->opt.direct != 0 || c->tree.L < 2;
   if (timing) cudaEventRecord(c->ev[0], st);
   if (!direct) {
     launch_upward(c, s, st);
+    if (distributed) {  // partial multipoles of the owned subtrees -> every cell's full multipole
+      if (timing) cudaEventRecord(c->ev[5], st);
+      const size_t off = (size_t)c->tree.lvl_off[2] * c->NC;
+      comm_allreduce_f32(c, reinterpret_cast<float*>(c->Mx.get() + off), 2 * (c->Mx.n - off), st);
+      if (timing) cudaEventRecord(c->ev[6], st);
+    }
     if (timing) cudaEventRecord(c->ev[1], st);
-    launch_m2l(c, *s.set, *t.set, st);
-    launch_downward(c, *t.set, st);
+    const int* tcnt = t.cnt ? t.cnt : t.set->cell_cnt.get();
+    launch_m2l(c, s.set->cell_cnt.get(), tcnt, st);
+    if (timing) cudaEventRecord(c->ev[8], st);
+    launch_downward(c, tcnt, st);
     if (timing) cudaEventRecord(c->ev[2], st);
   } else if (timing) {
     cudaEventRecord(c->ev[1], st);
+    cudaEventRecord(c->ev[8], st);
     cudaEventRecord(c->ev[2], st);
   }
   launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
@@ -144,34 +208,42 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     launch_l2p(c, t, acc, st);
   }
   if (timing) cudaEventRecord(c->ev[4], st);
+  c->timed_comm = timing && distributed && !direct;
 }
 
+// y = op(x) on this rank's panels; x, y local slices (pointers are shifted so that the kernels'
+// global tree indices land in the slice)
 void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_t st, bool timing) {
-  TgtArg t;
-  t.set = &c->pan;
+  TgtArg t = own_targets(c, false);
+  float* yg = y - c->pan_lo;
+  const float* xg = x - c->pan_lo;
   Outputs o;
   if (op == FMMBEM_OP_SINGLE) {
-    o.pot.y = y;
+    o.pot.y = yg;
     o.pot.b = (float)(1.0 / FOUR_PI);
   } else {
-    o.dn.y = y;
+    o.dn.y = yg;
     if (op == FMMBEM_OP_KPRIME) {
       o.dn.b = (float)(1.0 / FOUR_PI);
     } else {  // A = I - f K'
-      o.dn.x = x;
+      o.dn.x = xg;
       o.dn.ax = 1.f;
       o.dn.b = (float)(-c->f / FOUR_PI);
     }
   }
-  fmm_eval(c, t, kp_src(c, x), o, /*self=*/true, /*check=*/false, st, timing);
+  bool dist = false;
+  if (timing) cudaEventRecord(c->ev[7], st);
+  SrcArg s = kp_src(c, x, st, &dist);
+  fmm_eval(c, t, s, o, /*self=*/true, /*check=*/false, st, timing, dist);
 }
 
 void apply_A(fmmbem_ctx* c, const float* x, float* y, cudaStream_t s) { apply_op(c, FMMBEM_OP_A, x, y, s, false); }
 
 void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
   if (c->have_fields) return;
-  c->En.alloc(c->np);
-  c->psi.alloc(c->np);
+  const int64_t n = c->n_own();
+  c->En.alloc(std::max<int64_t>(n, 1));
+  c->psi.alloc(std::max<int64_t>(n, 1));
   if (c->nc == 0) {
     c->En.zero(st);
     c->psi.zero(st);
@@ -179,29 +251,29 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
     return;
   }
   FMM_CUDA(cudaMemsetAsync(c->flag.get(), 0, sizeof(int), st));
-  TgtArg t;
-  t.set = &c->pan;
-  SrcArg s;
+  TgtArg t = own_targets(c, false);
+  SrcArg s;  // charges are replicated on every rank: full upward sweep, no exchange
   s.set = &c->chg;
   Outputs o;
-  o.dn.y = c->En.get();
+  o.dn.y = c->En.get() - c->pan_lo;
   o.dn.b = (float)(1.0 / (FOUR_PI * c->eps_in));  // E_n carries 1/eps_I (Eq. 1, reading A2)
   if (c->K == 1) {
-    o.pot.y = c->psi.get();
+    o.pot.y = c->psi.get() - c->pan_lo;
     o.pot.b = (float)(1.0 / FOUR_PI);
   }
-  fmm_eval(c, t, s, o, false, true, st, false);
+  fmm_eval(c, t, s, o, false, true, st, false, false);
   if (c->K > 1) {
     DevBuf<float> psiq;
     psiq.alloc(c->quad.n);
-    TgtArg tq;
-    tq.set = &c->quad;
+    TgtArg tq = own_targets(c, true);
     Outputs oq;
     oq.pot.y = psiq.get();
     oq.pot.b = (float)(1.0 / FOUR_PI);
-    fmm_eval(c, tq, s, oq, false, true, st, false);
-    k_quad_reduce<<<ceil_div(c->np, 256), 256, 0, st>>>(c->np, c->K, psiq.get(), c->quad.pos.get(), c->pan.pos.get(),
-                                                        c->psi.get());
+    fmm_eval(c, tq, s, oq, false, true, st, false, false);
+    if (n > 0)
+      k_quad_reduce<<<ceil_div(n, 256), 256, 0, st>>>(n, c->K, psiq.get() + c->pan_lo * c->K,
+                                                      c->quad.pos.get() + c->pan_lo * c->K,
+                                                      c->pan.pos.get() + c->pan_lo, c->psi.get());
     FMM_CHECK_LAUNCH();
     FMM_CUDA(cudaStreamSynchronize(st));
   }
@@ -210,6 +282,57 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
   FMM_CUDA(cudaStreamSynchronize(st));
   if (flag) throw Error(FMMBEM_E_COINCIDENT, "a charge coincides with a panel quadrature point");
   c->have_fields = true;
+}
+
+// Multi-GPU partition: contiguous Morton ranges of leaves with equal estimated cost
+// ("equally distribute the Morton-indexed boxes", weighted by work instead of count).
+void partition(fmmbem_ctx* c, cudaStream_t st) {
+  const Tree& T = c->tree;
+  const int nl = (int)T.n_leaves;
+  DevBuf<double> cost;
+  DevBuf<long long> p2p;
+  cost.alloc(std::max(nl, 1));
+  p2p.alloc(std::max(nl, 1));
+  const PointSet& S = (c->K == 1) ? c->pan : c->quad;
+  k_leaf_cost<<<ceil_div(nl, 256), 256, 0, st>>>(nl, (int)T.lvl_off[T.L], c->pan.begin.get(), T.nbr_off.get(),
+                                                 T.nbr_idx.get(), T.m2l_off.get(), cost.get(), p2p.get());
+  FMM_CHECK_LAUNCH();
+  (void)S;
+  std::vector<double> hc(nl);
+  std::vector<long long> hp(nl);
+  std::vector<int> beg(nl + 1);
+  FMM_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), nl * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(hp.data(), p2p.get(), nl * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(beg.data(), c->pan.begin.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaStreamSynchronize(st));
+  const int R = c->nranks;
+  std::vector<int64_t> bounds(R + 1);
+  split_costs(hc.data(), nl, R, bounds.data());
+  c->leaf_lo = (int)bounds[c->rank];
+  c->leaf_hi = (int)bounds[c->rank + 1];
+  c->pan_offs.assign(R + 1, 0);
+  for (int r = 0; r <= R; ++r) c->pan_offs[r] = beg[bounds[r]];
+  c->pan_lo = c->pan_offs[c->rank];
+  c->pan_hi = c->pan_offs[c->rank + 1];
+  long long own = 0;
+  for (int k = c->leaf_lo; k < c->leaf_hi; ++k) own += hp[k];
+  c->p2p_inter_kp = own - (int64_t)c->n_own() * (c->K == 1 ? 1 : c->K);
+  // subtree counts of the owned points
+  for (int q = 0; q < 2; ++q) {
+    if (q == 1 && c->K == 1) continue;
+    DevBuf<int>& cnt = q ? c->quad_own_cnt : c->pan_own_cnt;
+    cnt.alloc(T.n_cells);
+    cnt.zero(st);
+    k_own_leaf_counts<<<ceil_div(nl, 256), 256, 0, st>>>(nl, c->pan.begin.get(), q ? c->K : 1, (int)T.lvl_off[T.L],
+                                                         c->leaf_lo, c->leaf_hi, cnt.get());
+    for (int l = T.L - 1; l >= 0; --l) {
+      int n = (int)(T.lvl_off[l + 1] - T.lvl_off[l]);
+      k_up_counts2<<<ceil_div(n, 256), 256, 0, st>>>(n, (int)T.lvl_off[l], T.child_begin.get(), T.child_end.get(),
+                                                     cnt.get());
+    }
+    FMM_CHECK_LAUNCH();
+  }
+  FMM_CUDA(cudaStreamSynchronize(st));
 }
 
 void fill_timing(fmmbem_ctx* c, bool direct) {
@@ -221,10 +344,20 @@ void fill_timing(fmmbem_ctx* c, bool direct) {
   std::memset(&T, 0, sizeof(T));
   T.gmres = g;
   T.upward = t[0];
-  T.m2l = t[1];
+  if (c->timed_comm) {
+    float tc = 0, ta = 0;
+    cudaEventElapsedTime(&tc, c->ev[5], c->ev[6]);  // multipole all-reduce
+    cudaEventElapsedTime(&ta, c->ev[7], c->ev[0]);  // x all-gather
+    T.comm = tc + ta;
+    T.upward -= tc;
+    T.total += ta;
+  }
+  float tm = 0;
+  cudaEventElapsedTime(&tm, c->ev[1], c->ev[8]);  // M2L alone; L2L is counted with L2P (downward)
+  T.m2l = tm;
   T.p2p = t[2];
-  T.l2p = t[3];
-  T.total = t[0] + t[1] + t[2] + t[3];
+  T.l2p = t[3] + (t[1] - tm);
+  T.total += t[0] + t[1] + t[2] + t[3];
   T.p2p_interactions = c->p2p_inter_kp;
   T.m2l_pairs = direct ? 0 : c->m2l_pairs_kp;
 }
@@ -286,7 +419,9 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
     throw Error(FMMBEM_E_INVALID, "quad_points must be 1, 3, 6 or 7");
   if (opt.near_mode != 0) throw Error(FMMBEM_E_INVALID, "near_mode = 1 (analytic near field) is not available yet");
   if (opt.self_term != 0) throw Error(FMMBEM_E_INVALID, "self_term = 1 is not available yet");
-  if (opt.nranks != 1 || opt.rank != 0) throw Error(FMMBEM_E_INVALID, "nranks > 1 is not available yet");
+  if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks) throw Error(FMMBEM_E_INVALID, "bad rank / nranks");
+  if (opt.nranks > 1 && !opt.nccl_id) throw Error(FMMBEM_E_INVALID, "nranks > 1 needs options.nccl_id");
+  if (opt.nranks > 1 && opt.direct) throw Error(FMMBEM_E_INVALID, "direct mode is single-GPU only");
   if (!(eps_in > 0) || !(eps_out > 0) || eps_in == eps_out || !std::isfinite(eps_in) || !std::isfinite(eps_out))
     throw Error(FMMBEM_E_INVALID, "need eps_in, eps_out > 0 and eps_in != eps_out");
   if (mesh->n_triangles < 1 || mesh->n_vertices < 3 || !mesh->xyz || !mesh->tri)
@@ -375,8 +510,24 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   c->Lx.alloc((size_t)c->tree.n_cells * c->NC);
   c->red.alloc(64);
   const PointSet& src = (c->K == 1) ? c->pan : c->quad;
+  c->rank = opt.rank;
+  c->nranks = opt.nranks;
+  c->leaf_lo = 0;
+  c->leaf_hi = (int)c->tree.n_leaves;
+  c->pan_lo = 0;
+  c->pan_hi = np;
+  c->pan_offs = {0, np};
   c->p2p_inter_kp = count_p2p(c, c->pan, src, true, c->opt.direct != 0 || c->tree.L < 2);
-  c->m2l_pairs_kp = (c->opt.direct != 0 || c->tree.L < 2) ? 0 : c->tree.m2l_pairs;
+  if (c->nranks > 1) {
+    comm_init(c, opt.nccl_id);
+    partition(c, s);
+  }
+  c->m2l_pairs_kp = 0;
+  if (!(c->opt.direct != 0 || c->tree.L < 2)) {
+    const int* tc = (c->nranks > 1) ? c->pan_own_cnt.get() : c->pan.cell_cnt.get();
+    if (rot_supported(c->P) && c->m2l_mode == 0) c->m2l_pairs_kp = m2l_work(c, src.cell_cnt.get(), tc, s).pairs;
+    else c->m2l_pairs_kp = c->tree.m2l_pairs;
+  }
   FMM_CUDA(cudaStreamSynchronize(s));
   *out = c;
   return FMMBEM_OK;
@@ -398,6 +549,10 @@ void fmmbem_destroy(fmmbem_ctx* c) {
   {
     DevGuard dg(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    try {
+      comm_destroy(c);
+    } catch (...) {
+    }
     for (auto& e : c->ev)
       if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -405,12 +560,28 @@ void fmmbem_destroy(fmmbem_ctx* c) {
   }
 }
 
-int64_t fmmbem_num_local_panels(const fmmbem_ctx* c) { return c ? c->np : 0; }
+int64_t fmmbem_num_local_panels(const fmmbem_ctx* c) { return c ? c->n_own() : 0; }
 
 fmmbem_status fmmbem_local_panel_ids(const fmmbem_ctx* c, int64_t* ids) {
   if (!c || !ids) return FMMBEM_E_INVALID;
-  std::memcpy(ids, c->pan_ids.data(), c->np * sizeof(int64_t));
+  std::memcpy(ids, c->pan_ids.data() + c->pan_lo, c->n_own() * sizeof(int64_t));
   return FMMBEM_OK;
+}
+
+fmmbem_status fmmbem_get_unique_id(void* id128) {
+  API_BEGIN
+  if (!id128) throw Error(FMMBEM_E_INVALID, "null id buffer");
+  comm_unique_id(id128);
+  return FMMBEM_OK;
+  API_END
+}
+
+fmmbem_status fmmbem_split_costs(const double* costs, int64_t n, int32_t parts, int64_t* bounds) {
+  API_BEGIN
+  if (!costs || !bounds || n < 0 || parts < 1) throw Error(FMMBEM_E_INVALID, "split_costs: bad arguments");
+  split_costs(costs, n, parts, bounds);
+  return FMMBEM_OK;
+  API_END
 }
 
 fmmbem_status fmmbem_matvec(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, void* stream) {
@@ -429,11 +600,12 @@ fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, f
   if (!c || !xh || !yh) throw Error(FMMBEM_E_INVALID, "matvec_host: null vectors");
   DevGuard dg(c->device);
   cudaStream_t st = c->stream;
-  c->tmp_x.alloc(c->np);
-  c->tmp_y.alloc(c->np);
-  FMM_CUDA(cudaMemcpyAsync(c->tmp_x.get(), xh, c->np * sizeof(float), cudaMemcpyHostToDevice, st));
+  const int64_t n = c->n_own();
+  c->tmp_x.alloc(std::max<int64_t>(n, 1));
+  c->tmp_y.alloc(std::max<int64_t>(n, 1));
+  FMM_CUDA(cudaMemcpyAsync(c->tmp_x.get(), xh, n * sizeof(float), cudaMemcpyHostToDevice, st));
   apply_op(c, op, c->tmp_x.get(), c->tmp_y.get(), st, true);
-  FMM_CUDA(cudaMemcpyAsync(yh, c->tmp_y.get(), c->np * sizeof(float), cudaMemcpyDeviceToHost, st));
+  FMM_CUDA(cudaMemcpyAsync(yh, c->tmp_y.get(), n * sizeof(float), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
   return FMMBEM_OK;
   API_END
@@ -444,8 +616,9 @@ fmmbem_status fmmbem_charge_fields(fmmbem_ctx* c, float* En, float* psi) {
   if (!c) throw Error(FMMBEM_E_INVALID, "null ctx");
   DevGuard dg(c->device);
   ensure_fields(c, c->stream);
-  if (En) FMM_CUDA(cudaMemcpyAsync(En, c->En.get(), c->np * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
-  if (psi) FMM_CUDA(cudaMemcpyAsync(psi, c->psi.get(), c->np * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  const size_t nb = c->n_own() * sizeof(float);
+  if (En) FMM_CUDA(cudaMemcpyAsync(En, c->En.get(), nb, cudaMemcpyDeviceToDevice, c->stream));
+  if (psi) FMM_CUDA(cudaMemcpyAsync(psi, c->psi.get(), nb, cudaMemcpyDeviceToDevice, c->stream));
   FMM_CUDA(cudaStreamSynchronize(c->stream));
   return FMMBEM_OK;
   API_END
@@ -462,15 +635,16 @@ fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* c, fmmbem_bibee v, float* sig, fmm
   const double d = 1.0 - c->f * s;
   if (d == 0.0) throw Error(FMMBEM_E_INVALID, "1 - f s == 0 (SPEC S:383)");
   DevBuf<float> tmp;
+  const int64_t n = c->n_own();
   float* sh = sig;
   if (!sh) {
-    tmp.alloc(c->np);
+    tmp.alloc(std::max<int64_t>(n, 1));
     sh = tmp.get();
   }
   // sigma_hat = f E / (1 - f s)   (Eq. 7 with K' -> s I, reading A3)
-  k_scale<<<ceil_div(c->np, 256), 256, 0, st>>>(sh, c->En.get(), c->np, (float)(c->f / d));
+  if (n > 0) k_scale<<<ceil_div(n, 256), 256, 0, st>>>(sh, c->En.get(), n, (float)(c->f / d));
   FMM_CHECK_LAUNCH();
-  const double e = 0.5 * dot_weighted(c, c->np, sh, c->psi.get(), c->pan.pos.get(), st);  // A20
+  const double e = 0.5 * dot_weighted(c, n, sh, c->psi.get(), c->pan.pos.get() + c->pan_lo, st);  // A20
   out->dG_internal = e;
   out->dG_kcal_mol = e * KCAL;
   out->iterations = 0;
@@ -492,13 +666,14 @@ fmmbem_status fmmbem_solve(fmmbem_ctx* c, const fmmbem_solve_options* so, float*
   ensure_fields(c, st);
   if (c->red.n < (size_t)o.restart + 2) c->red.alloc(o.restart + 2 + 64);
   DevBuf<float> b, xs;
-  b.alloc(c->np);
+  const int64_t n = c->n_own();
+  b.alloc(std::max<int64_t>(n, 1));
   float* x = sigma;
   if (!x) {
-    xs.alloc(c->np);
+    xs.alloc(std::max<int64_t>(n, 1));
     x = xs.get();
   }
-  k_scale<<<ceil_div(c->np, 256), 256, 0, st>>>(b.get(), c->En.get(), c->np, (float)c->f);  // b = f E
+  if (n > 0) k_scale<<<ceil_div(n, 256), 256, 0, st>>>(b.get(), c->En.get(), n, (float)c->f);  // b = f E
   FMM_CHECK_LAUNCH();
   if (hist)
     for (int i = 0; i <= o.max_iters; ++i) hist[i] = -1.0;
@@ -510,7 +685,7 @@ fmmbem_status fmmbem_solve(fmmbem_ctx* c, const fmmbem_solve_options* so, float*
   cudaEventRecord(e0, st);
   fmmbem_status stt = gmres_solve(c, b.get(), x, o.tol, o.restart, o.max_iters, o.x0_dev, hist, &its, &rr, st);
   cudaEventRecord(e1, st);
-  const double e = 0.5 * dot_weighted(c, c->np, x, c->psi.get(), c->pan.pos.get(), st);
+  const double e = 0.5 * dot_weighted(c, n, x, c->psi.get(), c->pan.pos.get() + c->pan_lo, st);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -534,12 +709,20 @@ fmmbem_status fmmbem_reaction_potential(fmmbem_ctx* c, const float* sigma, doubl
   DevBuf<double> yd;
   y.alloc(c->nc);
   yd.alloc(c->nc);
-  TgtArg t;
+  TgtArg t;  // every charge, on every rank (diagnostic path, replicated after the all-gather)
   t.set = &c->chg;
   Outputs o;
   o.pot.y = y.get();
   o.pot.b = (float)(1.0 / FOUR_PI);
-  fmm_eval(c, t, kp_src(c, sigma), o, false, false, st, false);
+  SrcArg s;
+  s.set = (c->K == 1) ? &c->pan : &c->quad;
+  s.x = sigma;
+  if (c->nranks > 1) {
+    c->xfull.alloc(c->np);
+    comm_allgatherv_f32(c, sigma, c->xfull.get(), c->pan_offs, st);
+    s.x = c->xfull.get();
+  }
+  fmm_eval(c, t, s, o, false, false, st, false, false);
   k_unpermute<<<ceil_div(c->nc, 256), 256, 0, st>>>(c->nc, c->chg_ids.get(), y.get(), yd.get());
   FMM_CHECK_LAUNCH();
   FMM_CUDA(cudaMemcpyAsync(phi, yd.get(), c->nc * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -8,7 +8,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "kernels.cuh"
@@ -103,6 +105,26 @@ void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const st
           "ncclBroadcast");
   }
   check(api().groupEnd(), "ncclGroupEnd");
+}
+
+// Contiguous split of n weighted items into `parts` ranges of (nearly) equal total weight:
+// bounds[0] = 0, bounds[parts] = n, bounds[r] = first index whose prefix sum reaches r/parts of
+// the total.  Pure host arithmetic, identical on every rank for identical inputs.
+void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds) {
+  std::vector<double> pre(n + 1, 0.0);
+  for (int64_t i = 0; i < n; ++i) pre[i + 1] = pre[i] + (cost[i] > 0 ? cost[i] : 0.0);
+  const double tot = pre[n];
+  bounds[0] = 0;
+  int64_t k = 0;
+  for (int r = 1; r < parts; ++r) {
+    const double goal = tot * (double)r / (double)parts;
+    while (k < n && pre[k + 1] <= goal) ++k;
+    // choose the closer of k and k+1 as the cut
+    int64_t cut = k;
+    if (k < n && (goal - pre[k]) > (pre[k + 1] - goal)) cut = k + 1;
+    bounds[r] = std::max<int64_t>(cut, bounds[r - 1]);
+  }
+  bounds[parts] = n;
 }
 
 }  // namespace fmm

@@ -39,8 +39,8 @@ struct Tree {
 
 // compacted M2L work for one (source set, target set) pair: rows = target cells
 struct M2LWork {
-  const PointSet* src = nullptr;
-  const PointSet* tgt = nullptr;
+  const int* src = nullptr;  // source / target subtree-count arrays that define the work
+  const int* tgt = nullptr;
   int64_t pairs = 0, rows = 0;
   DevBuf<int> idx;   // [pairs] source cells
   DevBuf<int> cell;  // [rows] target cells
@@ -50,6 +50,7 @@ struct M2LWork {
 // P2P work items (leaf, first target, count) of one target set
 struct P2PItems {
   const PointSet* tgt = nullptr;
+  int leaf_lo = 0, leaf_hi = 0;
   int64_t n = 0;
   DevBuf<int4> items;
 };
@@ -96,7 +97,17 @@ struct fmmbem_ctx {
   int m2l_mode = 0;  // 0 = rotation O(P^3) when available, 1 = plain O(P^4)
   int64_t p2p_inter_kp = 0, p2p_inter_chg = 0;  // exact interaction counts
   int64_t m2l_pairs_kp = 0;
+  // multi-GPU partition: this rank owns leaves [leaf_lo, leaf_hi) and the panels
+  // [pan_lo, pan_hi) of the tree order; pan_offs[r] = first panel of rank r
   void* comm = nullptr;  // ncclComm_t (nranks > 1)
+  int rank = 0, nranks = 1;
+  int leaf_lo = 0, leaf_hi = 0;
+  int64_t pan_lo = 0, pan_hi = 0;
+  std::vector<int64_t> pan_offs;
+  fmm::DevBuf<int> pan_own_cnt, quad_own_cnt;  // subtree counts of owned points
+  fmm::DevBuf<float> xfull;                    // all-gathered source weights
+  int64_t n_own() const { return pan_hi - pan_lo; }
   fmmbem_timing last{};
   cudaEvent_t ev[10] = {};
+  bool timed_comm = false;
 };

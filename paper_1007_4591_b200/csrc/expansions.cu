@@ -63,11 +63,11 @@ __device__ __forceinline__ void p2m_column(float* slot, const float4* __restrict
 
 template <int P>
 __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
-                                              const int* __restrict__ beg, float inv_w, int leaf_off,
+                                              const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               float2* __restrict__ M) {
   constexpr int NC = P * (P + 1) / 2;
   __shared__ float sv[2 * NC * 33];
-  const int leaf = blockIdx.x;
+  const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
@@ -86,11 +86,11 @@ __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, co
 
 template <int P>
 __global__ void __launch_bounds__(32) k_l2p_t(const float4* __restrict__ pos, const float4* __restrict__ nrm,
-                                              const int* __restrict__ beg, float inv_w, int leaf_off,
+                                              const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               const float2* __restrict__ Lx, OutArg pot, OutArg dn) {
   constexpr int NC = P * (P + 1) / 2;
   __shared__ float2 sl[NC + 1];
-  const int leaf = blockIdx.x;
+  const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
@@ -157,24 +157,26 @@ __global__ void __launch_bounds__(32) k_l2p_t(const float4* __restrict__ pos, co
 bool exp_specialised(int P) { return P == 8 || P == 10 || P == 12 || P == 14; }
 
 void launch_p2m_t(int P, int grid, const float4* pos, const float* x, int div, const int* beg, float inv_w,
-                  int leaf_off, float2* M, cudaStream_t st) {
+                  int leaf_off, int leaf0, float2* M, cudaStream_t st) {
+  if (grid <= 0) return;
   switch (P) {
-    case 8: k_p2m_t<8><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, M); break;
-    case 10: k_p2m_t<10><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, M); break;
-    case 12: k_p2m_t<12><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, M); break;
-    case 14: k_p2m_t<14><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, M); break;
+    case 8: k_p2m_t<8><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
+    case 10: k_p2m_t<10><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
+    case 12: k_p2m_t<12><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
+    case 14: k_p2m_t<14><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
     default: throw Error(FMMBEM_E_INVALID, "P2M not specialised for this P");
   }
   FMM_CHECK_LAUNCH();
 }
 
 void launch_l2p_t(int P, int grid, const float4* pos, const float4* nrm, const int* beg, float inv_w, int leaf_off,
-                  const float2* Lx, const OutArg& pot, const OutArg& dn, cudaStream_t st) {
+                  int leaf0, const float2* Lx, const OutArg& pot, const OutArg& dn, cudaStream_t st) {
+  if (grid <= 0) return;
   switch (P) {
-    case 8: k_l2p_t<8><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, Lx, pot, dn); break;
-    case 10: k_l2p_t<10><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, Lx, pot, dn); break;
-    case 12: k_l2p_t<12><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, Lx, pot, dn); break;
-    case 14: k_l2p_t<14><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, Lx, pot, dn); break;
+    case 8: k_l2p_t<8><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
+    case 10: k_l2p_t<10><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
+    case 12: k_l2p_t<12><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
+    case 14: k_l2p_t<14><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
     default: throw Error(FMMBEM_E_INVALID, "L2P not specialised for this P");
   }
   FMM_CHECK_LAUNCH();

@@ -55,9 +55,9 @@ __device__ __forceinline__ float2 getc(const float2* X, int n, int m) {
 // CTA per leaf; thread (g, m): source group g (8 groups), order m (16 slots).
 __global__ void __launch_bounds__(128) k_p2m(const float4* __restrict__ pos, const float* __restrict__ x, int div,
                                              const int* __restrict__ beg, int P, float inv_w, int leaf_off,
-                                             float2* __restrict__ M) {
+                                             int leaf0, float2* __restrict__ M) {
   __shared__ float2 sm[8][16][MAX_TERMS];
-  const int leaf = blockIdx.x;
+  const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int g = threadIdx.x >> 4, m = threadIdx.x & 15;
@@ -284,9 +284,9 @@ __global__ void __launch_bounds__(64) k_l2l(int lvl_off, int P, const int* __res
 // CTA per leaf; 8 targets at a time, 16 lanes (orders m) per target, reduced by shuffles.
 __global__ void __launch_bounds__(128) k_l2p(const float4* __restrict__ pos, const float4* __restrict__ nrm,
                                              const int* __restrict__ beg, int P, float inv_w, int leaf_off,
-                                             const float2* __restrict__ Lx, OutArg pot, OutArg dn) {
+                                             int leaf0, const float2* __restrict__ Lx, OutArg pot, OutArg dn) {
   __shared__ float2 sl[MAX_TERMS * (MAX_TERMS + 1) / 2];
-  const int leaf = blockIdx.x;
+  const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int NC = P * (P + 1) / 2;
@@ -425,30 +425,34 @@ void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
   if (L < 2) return;
   c->Mx.zero(st);
   const PointSet& S = *s.set;
-  if (exp_specialised(P)) {
-    launch_p2m_t(P, (int)T.n_leaves, S.pos.get(), s.x, S.div, S.begin.get(), (float)(1.0 / T.width(L)),
-                 (int)T.lvl_off[L], c->Mx.get(), st);
-  } else {
-    k_p2m<<<(int)T.n_leaves, 128, 0, st>>>(S.pos.get(), s.x, S.div, S.begin.get(), P, (float)(1.0 / T.width(L)),
-                                           (int)T.lvl_off[L], c->Mx.get());
-    FMM_CHECK_LAUNCH();
+  const int lo = s.leaf_lo, hi = s.leaf_hi < 0 ? (int)T.n_leaves : s.leaf_hi;
+  const int* cnt = s.cnt ? s.cnt : S.cell_cnt.get();
+  if (hi > lo) {
+    if (exp_specialised(P)) {
+      launch_p2m_t(P, hi - lo, S.pos.get(), s.x, S.div, S.begin.get(), (float)(1.0 / T.width(L)),
+                   (int)T.lvl_off[L], lo, c->Mx.get(), st);
+    } else {
+      k_p2m<<<hi - lo, 128, 0, st>>>(S.pos.get(), s.x, S.div, S.begin.get(), P, (float)(1.0 / T.width(L)),
+                                     (int)T.lvl_off[L], lo, c->Mx.get());
+      FMM_CHECK_LAUNCH();
+    }
   }
   for (int l = L - 1; l >= 2; --l) {
     int n = (int)(T.lvl_off[l + 1] - T.lvl_off[l]);
     k_m2m<<<n, 64, 16 * NC * sizeof(float2), st>>>((int)T.lvl_off[l], P, T.child_begin.get(), T.child_end.get(),
-                                                   T.key.get(), S.cell_cnt.get(), c->Mx.get());
+                                                   T.key.get(), cnt, c->Mx.get());
     FMM_CHECK_LAUNCH();
   }
 }
 
-void launch_m2l(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStream_t st) {
+void launch_m2l(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStream_t st) {
   const Tree& T = c->tree;
   const int L = T.L, P = c->P;
   if (L < 2) return;
   c->Lx.zero(st);
   if (c->m2l_mode == 0 && rot_supported(P)) {
     init_rot_tables();
-    launch_m2l_rot(c, m2l_work(c, src, tgt, st), st);
+    launch_m2l_rot(c, m2l_work(c, src_cnt, tgt_cnt, st), st);
     return;
   }
   const int n = (int)(T.n_cells - T.lvl_off[2]);
@@ -458,19 +462,19 @@ void launch_m2l(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStr
     FMM_CUDA(cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     attr = true;
   }
-  k_m2l<<<n, M2L_TPB, smem, st>>>((int)T.lvl_off[2], P, T.m2l_off.get(), T.m2l_idx.get(), T.key.get(),
-                                   src.cell_cnt.get(), tgt.cell_cnt.get(), c->Mx.get(), c->Itab.get(), c->Lx.get());
+  k_m2l<<<n, M2L_TPB, smem, st>>>((int)T.lvl_off[2], P, T.m2l_off.get(), T.m2l_idx.get(), T.key.get(), src_cnt,
+                                   tgt_cnt, c->Mx.get(), c->Itab.get(), c->Lx.get());
   FMM_CHECK_LAUNCH();
 }
 
-void launch_downward(fmmbem_ctx* c, const PointSet& tgt, cudaStream_t st) {
+void launch_downward(fmmbem_ctx* c, const int* tgt_cnt, cudaStream_t st) {
   const Tree& T = c->tree;
   const int L = T.L, P = c->P, NC = c->NC;
   if (L < 2) return;
   for (int l = 2; l < L; ++l) {
     int n = (int)(T.lvl_off[l + 2] - T.lvl_off[l + 1]);
-    k_l2l<<<n, 64, 2 * NC * sizeof(float2), st>>>((int)T.lvl_off[l + 1], P, T.parent.get(), T.key.get(),
-                                              tgt.cell_cnt.get(), c->Lx.get());
+    k_l2l<<<n, 64, 2 * NC * sizeof(float2), st>>>((int)T.lvl_off[l + 1], P, T.parent.get(), T.key.get(), tgt_cnt,
+                                                  c->Lx.get());
     FMM_CHECK_LAUNCH();
   }
 }
@@ -480,13 +484,15 @@ void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t s
   const int L = T.L;
   if (L < 2) return;
   const PointSet& S = *t.set;
+  const int lo = t.leaf_lo, hi = t.leaf_hi < 0 ? (int)T.n_leaves : t.leaf_hi;
+  if (hi <= lo) return;
   if (exp_specialised(c->P)) {
-    launch_l2p_t(c->P, (int)T.n_leaves, S.pos.get(), S.nrm.get(), S.begin.get(), (float)(1.0 / T.width(L)),
-                 (int)T.lvl_off[L], c->Lx.get(), o.pot, o.dn, st);
+    launch_l2p_t(c->P, hi - lo, S.pos.get(), S.nrm.get(), S.begin.get(), (float)(1.0 / T.width(L)),
+                 (int)T.lvl_off[L], lo, c->Lx.get(), o.pot, o.dn, st);
     return;
   }
-  k_l2p<<<(int)T.n_leaves, 128, 0, st>>>(S.pos.get(), S.nrm.get(), S.begin.get(), c->P, (float)(1.0 / T.width(L)),
-                                         (int)T.lvl_off[L], c->Lx.get(), o.pot, o.dn);
+  k_l2p<<<hi - lo, 128, 0, st>>>(S.pos.get(), S.nrm.get(), S.begin.get(), c->P, (float)(1.0 / T.width(L)),
+                                 (int)T.lvl_off[L], lo, c->Lx.get(), o.pot, o.dn);
   FMM_CHECK_LAUNCH();
 }
 

@@ -1,5 +1,7 @@
 // kernels.cuh -- launch interfaces shared by the .cu files of libfmmbem.
 #pragma once
+#include <vector>
+
 #include "ctx.h"
 
 namespace fmm {
@@ -13,14 +15,21 @@ struct OutArg {
 };
 
 // A source set for one apply: weight of point j = (x ? x[j / div] : 1) * pos[j].w
+// A leaf range [leaf_lo, leaf_hi) (hi < 0: all leaves) restricts the work to this rank's part
+// (multi-GPU); cnt = per-cell subtree point counts used to skip empty cells
+// (nullptr: the set's full counts).
 struct SrcArg {
   const PointSet* set = nullptr;
   const float* x = nullptr;
+  int leaf_lo = 0, leaf_hi = -1;
+  const int* cnt = nullptr;
 };
 
 // targets: positions (+ normals for normal-derivative outputs)
 struct TgtArg {
   const PointSet* set = nullptr;
+  int leaf_lo = 0, leaf_hi = -1;
+  const int* cnt = nullptr;
 };
 
 struct Outputs {
@@ -34,28 +43,38 @@ void build_tree(fmmbem_ctx* c, const double* cen, const double* nrm, const doubl
 // near field; writes y = ax x + b raw (overwrites)
 void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
                 bool direct, cudaStream_t st);
-const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t);
+const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi);
+
+// multi-GPU (comm.cu); all no-ops when nranks == 1
+void comm_unique_id(void* id128);
+void comm_init(fmmbem_ctx* c, const void* id128);
+void comm_destroy(fmmbem_ctx* c);
+void comm_allreduce_f32(fmmbem_ctx* c, float* buf, size_t n, cudaStream_t s);
+void comm_allreduce_f64(fmmbem_ctx* c, double* buf, size_t n, cudaStream_t s);
+void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const std::vector<int64_t>& offs,
+                         cudaStream_t s);
+void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds);
 // exact interaction count of launch_p2p(t, s) (list mode) -- setup-time helper
 int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct);
 
 // far field (expansions in c->Mx / c->Lx); l2p accumulates y += b far
 void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
-void launch_m2l(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStream_t st);
-void launch_downward(fmmbem_ctx* c, const PointSet& tgt, cudaStream_t st);
+void launch_m2l(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStream_t st);
+void launch_downward(fmmbem_ctx* c, const int* tgt_cnt, cudaStream_t st);
 void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t st);
 void init_tables(fmmbem_ctx* c);
 
 // order-specialised P2M / L2P (expansions.cu)
 bool exp_specialised(int P);
 void launch_p2m_t(int P, int grid, const float4* pos, const float* x, int div, const int* beg, float inv_w,
-                  int leaf_off, float2* M, cudaStream_t st);
+                  int leaf_off, int leaf0, float2* M, cudaStream_t st);
 void launch_l2p_t(int P, int grid, const float4* pos, const float4* nrm, const int* beg, float inv_w, int leaf_off,
-                  const float2* Lx, const OutArg& pot, const OutArg& dn, cudaStream_t st);
+                  int leaf0, const float2* Lx, const OutArg& pot, const OutArg& dn, cudaStream_t st);
 
 // rotation-accelerated M2L (m2l_rot.cu)
 bool rot_supported(int P);
 void init_rot_tables();
-const M2LWork& m2l_work(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStream_t st);
+const M2LWork& m2l_work(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStream_t st);
 void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st);
 void scan_ints(const int* in, int* out, int n, cudaStream_t s);  // exclusive
 
@@ -67,6 +86,6 @@ fmmbem_status gmres_solve(fmmbem_ctx* c, const float* b, float* x, double tol, i
 
 // one full FMM (or direct) evaluation of targets t from sources s
 void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
-              cudaStream_t st, bool timing);
+              cudaStream_t st, bool timing, bool distributed);
 
 }  // namespace fmm

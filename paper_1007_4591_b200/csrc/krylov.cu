@@ -91,9 +91,16 @@ void gemv_t(fmmbem_ctx* c, const float* V, int64_t ld, int nvec, int64_t n, cons
   int nb = nblocks(n);
   size_t need = (size_t)nb * nvec;
   if (c->part.n < need) c->part.alloc(need);
-  k_gemv_t<<<nb, RB, 0, s>>>(V, ld, nvec, n, w, wt, c->part.get());
-  k_reduce_part<<<nvec, RB, 0, s>>>(nb, nvec, c->part.get(), h, acc ? 1 : 0);
+  if (nb > 0) {
+    k_gemv_t<<<nb, RB, 0, s>>>(V, ld, nvec, n, w, wt, c->part.get());
+    k_reduce_part<<<nvec, RB, 0, s>>>(nb, nvec, c->part.get(), h, acc ? 1 : 0);
+  } else if (!acc) {
+    FMM_CUDA(cudaMemsetAsync(h, 0, nvec * sizeof(double), s));
+  }
   FMM_CHECK_LAUNCH();
+  // distributed vectors: every rank holds a slice; the FP64 partial dots are summed over ranks
+  if (!acc) comm_allreduce_f64(c, h, nvec, s);
+  else throw Error(FMMBEM_E_INVALID, "accumulating distributed dot not supported");
 }
 
 }  // namespace
@@ -112,11 +119,11 @@ void apply_A(fmmbem_ctx* c, const float* x, float* y, cudaStream_t s);  // api.c
 
 fmmbem_status gmres_solve(fmmbem_ctx* c, const float* b, float* x, double tol, int m, int max_iters,
                           const float* x0, double* hist, int* iters, double* relres, cudaStream_t s) {
-  const int64_t n = c->np;
+  const int64_t n = c->n_own();
   const int TB = 256;
-  const int gb = ceil_div(n, TB);
-  c->V.alloc((size_t)(m + 1) * n);
-  c->w.alloc(n);
+  const int gb = std::max(1, ceil_div(n, TB));
+  c->V.alloc(std::max<size_t>((size_t)(m + 1) * n, 1));
+  c->w.alloc(std::max<int64_t>(n, 1));
   c->hd.alloc(m + 2);
   if (c->red.n < 2) c->red.alloc(64);
   float* V = c->V.get();

@@ -339,21 +339,21 @@ void init_rot_tables() {
 
 // Build (or fetch) the compacted M2L work list for (src, tgt): rows = target cells at levels >= 2
 // with target points and at least one source cell holding source points.
-const M2LWork& m2l_work(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt, cudaStream_t st) {
+const M2LWork& m2l_work(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStream_t st) {
   for (auto& w : c->m2l_cache)
-    if (w->src == &src && w->tgt == &tgt) return *w;
+    if (w->src == src_cnt && w->tgt == tgt_cnt) return *w;
   const Tree& T = c->tree;
   auto w = std::make_unique<M2LWork>();
-  w->src = &src;
-  w->tgt = &tgt;
+  w->src = src_cnt;
+  w->tgt = tgt_cnt;
   const int off0 = (int)T.lvl_off[2];
   const int n = (int)(T.n_cells - off0);
   DevBuf<int> cnt, pos;
   cnt.alloc(2 * (n + 1));
   pos.alloc(2 * (n + 1));
   cnt.zero(st);
-  k_compact_count<<<ceil_div(n, 256), 256, 0, st>>>(n, off0, T.m2l_off.get(), T.m2l_idx.get(), src.cell_cnt.get(),
-                                                     tgt.cell_cnt.get(), cnt.get());
+  k_compact_count<<<ceil_div(n, 256), 256, 0, st>>>(n, off0, T.m2l_off.get(), T.m2l_idx.get(), src_cnt, tgt_cnt,
+                                                     cnt.get());
   k_row_flags<<<ceil_div(n, 256), 256, 0, st>>>(n, cnt.get(), cnt.get() + n + 1);
   FMM_CHECK_LAUNCH();
   scan_ints(cnt.get(), pos.get(), n + 1, st);                    // pair offsets
@@ -367,8 +367,8 @@ const M2LWork& m2l_work(fmmbem_ctx* c, const PointSet& src, const PointSet& tgt,
   w->idx.alloc(std::max(1, h[0]));
   w->cell.alloc(std::max(1, h[1]));
   w->off.alloc(h[1] + 1);
-  k_compact_fill<<<ceil_div(n, 256), 256, 0, st>>>(n, off0, T.m2l_off.get(), T.m2l_idx.get(), src.cell_cnt.get(),
-                                                    pos.get(), w->idx.get(), w->cell.get(), w->off.get());
+  k_compact_fill<<<ceil_div(n, 256), 256, 0, st>>>(n, off0, T.m2l_off.get(), T.m2l_idx.get(), src_cnt, pos.get(),
+                                                    w->idx.get(), w->cell.get(), w->off.get());
   FMM_CHECK_LAUNCH();
   FMM_CUDA(cudaMemcpyAsync(w->off.get() + h[1], &h[0], sizeof(int), cudaMemcpyHostToDevice, st));
   FMM_CUDA(cudaStreamSynchronize(st));

@@ -281,31 +281,33 @@ __global__ void k_item_count(int nl, const int* __restrict__ tbeg, int chunk, in
   if (k < nl) cnt[k] = (tbeg[k + 1] - tbeg[k] + chunk - 1) / chunk;
 }
 
-__global__ void k_item_fill(int nl, const int* __restrict__ tbeg, int chunk, const int* __restrict__ pos,
-                            int4* items) {
+__global__ void k_item_fill(int nl, const int* __restrict__ tbeg, int leaf0, int chunk,
+                            const int* __restrict__ pos, int4* items) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nl) return;
   const int b = tbeg[k], e = tbeg[k + 1];
   int w = pos[k];
-  for (int t = b; t < e; t += chunk) items[w++] = make_int4(k, t, min(chunk, e - t), 0);
+  for (int t = b; t < e; t += chunk) items[w++] = make_int4(leaf0 + k, t, min(chunk, e - t), 0);
 }
 
 }  // namespace
 
 // (leaf, target chunk) work items of one target set, built once and cached
-const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t) {
+const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi) {
   for (auto& w : c->p2p_cache)
-    if (w->tgt == &t) return *w;
-  const int nl = (int)c->tree.n_leaves;
+    if (w->tgt == &t && w->leaf_lo == leaf_lo && w->leaf_hi == leaf_hi) return *w;
+  const int nl = leaf_hi - leaf_lo;
   const int chunk = 32 * P2P_T;
   cudaStream_t st = c->stream;
   auto w = std::make_unique<P2PItems>();
   w->tgt = &t;
+  w->leaf_lo = leaf_lo;
+  w->leaf_hi = leaf_hi;
   DevBuf<int> cnt, pos;
   cnt.alloc(nl + 1);
   pos.alloc(nl + 1);
   cnt.zero(st);
-  k_item_count<<<ceil_div(nl, 256), 256, 0, st>>>(nl, t.begin.get(), chunk, cnt.get());
+  if (nl > 0) k_item_count<<<ceil_div(nl, 256), 256, 0, st>>>(nl, t.begin.get() + leaf_lo, chunk, cnt.get());
   FMM_CHECK_LAUNCH();
   scan_ints(cnt.get(), pos.get(), nl + 1, st);
   int n = 0;
@@ -313,7 +315,9 @@ const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t) {
   FMM_CUDA(cudaStreamSynchronize(st));
   w->n = n;
   w->items.alloc(std::max(1, n));
-  k_item_fill<<<ceil_div(nl, 256), 256, 0, st>>>(nl, t.begin.get(), chunk, pos.get(), w->items.get());
+  if (nl > 0)
+    k_item_fill<<<ceil_div(nl, 256), 256, 0, st>>>(nl, t.begin.get() + leaf_lo, leaf_lo, chunk, pos.get(),
+                                                    w->items.get());
   FMM_CHECK_LAUNCH();
   FMM_CUDA(cudaStreamSynchronize(st));
   c->p2p_cache.push_back(std::move(w));
@@ -325,7 +329,8 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   const Tree& T = c->tree;
   const bool pot = o.pot.y != nullptr, dn = o.dn.y != nullptr;
   if (!pot && !dn) return;
-  const P2PItems& items = p2p_items(c, *t.set);
+  const P2PItems& items =
+      p2p_items(c, *t.set, t.leaf_lo, t.leaf_hi < 0 ? (int)c->tree.n_leaves : t.leaf_hi);
   if (items.n == 0) return;
   P2PArgs a{};
   a.items = items.items.get();
