@@ -313,6 +313,13 @@ def main():
                    "d2h_bytes_per_step": 4 * n},
            "comm_ms": ph["comm"],
            "clocks": clocks}
+    if dist:  # per-rank breakdown (load balance of the domain decomposition)
+        mine = {"rank": rank, "n_local": s.n, "phases_ms": ph, "p2p_interactions": int(tm["p2p_interactions"]),
+                "m2l_pairs": int(tm["m2l_pairs"])}
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        out["per_rank"] = allr
+        out["m2l_pairs"] = int(sum(r["m2l_pairs"] for r in allr))
     if rank == 0 and world == 1 and not args.no_cpu:
         rows = np.random.default_rng(11).choice(n, args.cpu_rows, replace=False)
         y_ref, dt, cores, _ = oracle_sample(cfg, rows, x_global)

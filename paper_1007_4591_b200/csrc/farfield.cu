@@ -437,7 +437,13 @@ void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
       FMM_CHECK_LAUNCH();
     }
   }
+  const bool rot = c->m2l_mode == 0 && m2m_rot_supported(P);
+  if (rot) init_rot_tables();
   for (int l = L - 1; l >= 2; --l) {
+    if (rot) {  // Lx is free during the upward sweep: scratch for the per-child translations
+      launch_m2m_rot(c, l, cnt, c->Lx.get(), st);
+      continue;
+    }
     int n = (int)(T.lvl_off[l + 1] - T.lvl_off[l]);
     k_m2m<<<n, 64, 16 * NC * sizeof(float2), st>>>((int)T.lvl_off[l], P, T.child_begin.get(), T.child_end.get(),
                                                    T.key.get(), cnt, c->Mx.get());
@@ -471,7 +477,13 @@ void launch_downward(fmmbem_ctx* c, const int* tgt_cnt, cudaStream_t st) {
   const Tree& T = c->tree;
   const int L = T.L, P = c->P, NC = c->NC;
   if (L < 2) return;
+  const bool rot = c->m2l_mode == 0 && m2m_rot_supported(P);
+  if (rot) init_rot_tables();
   for (int l = 2; l < L; ++l) {
+    if (rot) {
+      launch_l2l_rot(c, l, tgt_cnt, st);
+      continue;
+    }
     int n = (int)(T.lvl_off[l + 2] - T.lvl_off[l + 1]);
     k_l2l<<<n, 64, 2 * NC * sizeof(float2), st>>>((int)T.lvl_off[l + 1], P, T.parent.get(), T.key.get(), tgt_cnt,
                                                   c->Lx.get());

@@ -76,6 +76,9 @@ bool rot_supported(int P);
 void init_rot_tables();
 const M2LWork& m2l_work(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStream_t st);
 void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st);
+bool m2m_rot_supported(int P);
+void launch_m2m_rot(fmmbem_ctx* c, int l, const int* scnt, float2* T, cudaStream_t st);
+void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st);
 void scan_ints(const int* in, int* out, int n, cudaStream_t s);  // exclusive
 
 // Krylov / reductions

@@ -238,6 +238,206 @@ __global__ void __launch_bounds__(32 * W) k_m2l_rot(int rows, const int* __restr
   }
 }
 
+// ---------------------------------------------------------------- M2M / L2L by rotation
+// Child-parent offsets are the 8 diagonals d = (+-1, +-1, +-1)/4 (parent-width units), |d| = sqrt(3)/4,
+// so the coaxial shift coefficients are compile-time constants.  Rotations (verified against the
+// direct translations):  multipoles  fwd = X1 Phi(t) X0 Phi(p + pi/2),  back = Phi(-p - pi/2) X1 Phi(-t) X0
+//                        locals      fwd = X3 Phi(t) X2 Phi(p + pi/2),  back = Phi(-p - pi/2) X3 Phi(-t) X2
+// (X0 = D^-1, X1 = D, X2 = D^T, X3 = D^-T; the Phi(-+pi/2) around the coaxial step cancel).
+constexpr float RHO8 = 0.43301270189221932f;  // sqrt(3)/4
+
+__host__ __device__ constexpr float powf_c(float b, int e) {
+  float r = 1.f;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+// per degree block: a <- XB Phi(zb) XA Phi(za) a   (conj: use conjugated phases)
+template <int n, int XA, int XB>
+__device__ __forceinline__ void rot_block(float (&ar)[n + 1], float (&ai)[n + 1], const float* zar, const float* zai,
+                                          const float* zbr, const float* zbi, float csa, float csb) {
+  float br[n + 1], bi[n + 1];
+#pragma unroll
+  for (int m = 1; m <= n; ++m) cmul_ip(ar[m], ai[m], zar[m], csa * zai[m]);
+  mat_block<n, XA>(ar, ai, br, bi);
+#pragma unroll
+  for (int m = 1; m <= n; ++m) cmul_ip(br[m], bi[m], zbr[m], csb * zbi[m]);
+  mat_block<n, XB>(br, bi, ar, ai);
+}
+
+// pass over degrees: (global src | slot) -> rot_block -> (slot | global dst (=, +=))
+template <int P, int n, int XA, int XB, int MODE>  // MODE 0: src -> slot, 1: slot -> dst (=), 2: slot -> dst (+=)
+__device__ __forceinline__ void rot_pass(const Slot& sl, const float2* __restrict__ src, float2* __restrict__ dst,
+                                         const float* zar, const float* zai, const float* zbr, const float* zbi,
+                                         float cs) {
+  constexpr int c0 = n * (n + 1) / 2;
+  float ar[n + 1], ai[n + 1];
+#pragma unroll
+  for (int m = 0; m <= n; ++m) {
+    if (MODE == 0) {
+      const float2 q = __ldg(src + c0 + m);
+      ar[m] = q.x;
+      ai[m] = q.y;
+    } else {
+      ar[m] = sl.re(c0 + m);
+      ai[m] = sl.im(c0 + m);
+    }
+  }
+  if (MODE == 0) {
+    rot_block<n, XA, XB>(ar, ai, zar, zai, zbr, zbi, 1.f, 1.f);
+#pragma unroll
+    for (int m = 0; m <= n; ++m) {
+      sl.re(c0 + m) = ar[m];
+      sl.im(c0 + m) = ai[m];
+    }
+  } else {
+    // back rotation: XB Phi(-t) XA, then Phi(-p - pi/2)
+    float br[n + 1], bi[n + 1];
+    mat_block<n, XA>(ar, ai, br, bi);
+#pragma unroll
+    for (int m = 1; m <= n; ++m) cmul_ip(br[m], bi[m], zbr[m], -zbi[m]);
+    mat_block<n, XB>(br, bi, ar, ai);
+#pragma unroll
+    for (int m = 0; m <= n; ++m) {
+      if (m > 0) cmul_ip(ar[m], ai[m], zar[m], -zai[m]);
+      if (MODE == 1) {
+        dst[c0 + m] = make_float2(ar[m], ai[m]);
+      } else {
+        float2 o = dst[c0 + m];
+        dst[c0 + m] = make_float2(o.x + ar[m], o.y + ai[m]);
+      }
+    }
+  }
+  (void)cs;
+  if constexpr (n + 1 < P) rot_pass<P, n + 1, XA, XB, MODE>(sl, src, dst, zar, zai, zbr, zbi, cs);
+}
+
+// coaxial M2M along +z by RHO8: M_n^k <- sum_{j=k}^{n} 2^-j M_j^k rho^(n-j)/(n-j)!
+template <int P, int k>
+__device__ __forceinline__ void coax_m2m(const Slot& sl) {
+  float tr[P - k], ti[P - k];
+#pragma unroll
+  for (int j = k; j < P; ++j) {
+    tr[j - k] = sl.re(j * (j + 1) / 2 + k);
+    ti[j - k] = sl.im(j * (j + 1) / 2 + k);
+  }
+#pragma unroll
+  for (int n = k; n < P; ++n) {
+    float re = 0.f, im = 0.f;
+#pragma unroll
+    for (int j = k; j <= n; ++j) {
+      constexpr float one = 1.f;
+      const float cf = one / powf_c(2.f, j) * powf_c(RHO8, n - j) / factf(n - j);
+      re = fmaf(cf, tr[j - k], re);
+      im = fmaf(cf, ti[j - k], im);
+    }
+    sl.re(n * (n + 1) / 2 + k) = re;
+    sl.im(n * (n + 1) / 2 + k) = im;
+  }
+  if constexpr (k + 1 < P) coax_m2m<P, k + 1>(sl);
+}
+
+// coaxial L2L along +z by RHO8: L_j^k <- 2^-(j+1) sum_{n=j}^{P-1} L_n^k rho^(n-j)/(n-j)!
+template <int P, int k>
+__device__ __forceinline__ void coax_l2l(const Slot& sl) {
+  float tr[P - k], ti[P - k];
+#pragma unroll
+  for (int n = k; n < P; ++n) {
+    tr[n - k] = sl.re(n * (n + 1) / 2 + k);
+    ti[n - k] = sl.im(n * (n + 1) / 2 + k);
+  }
+#pragma unroll
+  for (int j = k; j < P; ++j) {
+    float re = 0.f, im = 0.f;
+#pragma unroll
+    for (int n = j; n < P; ++n) {
+      const float cf = 1.f / powf_c(2.f, j + 1) * powf_c(RHO8, n - j) / factf(n - j);
+      re = fmaf(cf, tr[n - k], re);
+      im = fmaf(cf, ti[n - k], im);
+    }
+    sl.re(j * (j + 1) / 2 + k) = re;
+    sl.im(j * (j + 1) / 2 + k) = im;
+  }
+  if constexpr (k + 1 < P) coax_l2l<P, k + 1>(sl);
+}
+
+// phase powers of za = e^{i(p + pi/2)}, zb = e^{i t} for the octant of a child key
+template <int P>
+__device__ __forceinline__ void octant_phases(uint64_t key, float* zar, float* zai, float* zbr, float* zbi) {
+  const float sx = (key & 1) ? 1.f : -1.f, sy = (key & 2) ? 1.f : -1.f, sz = (key & 4) ? 1.f : -1.f;
+  const float r2 = 0.70710678118654752f;  // |(sx, sy)| / sqrt(2) normalisation
+  const float cp = sx * r2, sp = sy * r2;
+  const float ct = sz * 0.57735026918962576f, st = 0.81649658092772603f;  // cos t = sz/sqrt(3), sin t = sqrt(2/3)
+  const float ar1 = -sp, ai1 = cp;
+  zar[0] = 1.f;
+  zai[0] = 0.f;
+  zbr[0] = 1.f;
+  zbi[0] = 0.f;
+#pragma unroll
+  for (int m = 1; m < P; ++m) {
+    zar[m] = zar[m - 1] * ar1 - zai[m - 1] * ai1;
+    zai[m] = zar[m - 1] * ai1 + zai[m - 1] * ar1;
+    zbr[m] = zbr[m - 1] * ct - zbi[m - 1] * st;
+    zbi[m] = zbr[m - 1] * st + zbi[m - 1] * ct;
+  }
+}
+
+// thread per child cell at one level: T[child] = (translated child multipole); summed per parent below
+template <int P>
+__global__ void __launch_bounds__(32) k_m2m_rot(int c0, int n, const uint64_t* __restrict__ key,
+                                                const int* __restrict__ scnt, const float2* __restrict__ M,
+                                                float2* __restrict__ T) {
+  constexpr int NC = P * (P + 1) / 2;
+  __shared__ float sv[2 * NC * 33];
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  if (i >= n) return;
+  const int cell = c0 + i;
+  if (scnt[cell] == 0) return;
+  const Slot sl{sv + threadIdx.x};
+  float zar[P], zai[P], zbr[P], zbi[P];
+  octant_phases<P>(key[cell], zar, zai, zbr, zbi);
+  rot_pass<P, 0, 0, 1, 0>(sl, M + (size_t)cell * NC, nullptr, zar, zai, zbr, zbi, 1.f);
+  coax_m2m<P, 0>(sl);
+  rot_pass<P, 0, 0, 1, 1>(sl, nullptr, T + (size_t)cell * NC, zar, zai, zbr, zbi, 1.f);
+}
+
+// parent multipole = sum of its children's translated multipoles (fixed order)
+__global__ void k_m2m_sum(int c0, int n, int NC, const int* __restrict__ cb, const int* __restrict__ ce,
+                          const int* __restrict__ scnt, const float2* __restrict__ T, float2* __restrict__ M) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = t / NC, c = t - i * NC;
+  if (i >= n) return;
+  const int cell = c0 + i;
+  if (scnt[cell] == 0) return;
+  float2 s = make_float2(0.f, 0.f);
+  for (int ch = cb[cell]; ch < ce[cell]; ++ch) {
+    if (scnt[ch] == 0) continue;
+    const float2 v = T[(size_t)ch * NC + c];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  M[(size_t)cell * NC + c] = s;
+}
+
+// thread per child cell: L[child] += translated parent local expansion
+template <int P>
+__global__ void __launch_bounds__(32) k_l2l_rot(int c0, int n, const uint64_t* __restrict__ key,
+                                                const int* __restrict__ parent, const int* __restrict__ tcnt,
+                                                float2* __restrict__ Lx) {
+  constexpr int NC = P * (P + 1) / 2;
+  __shared__ float sv[2 * NC * 33];
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  if (i >= n) return;
+  const int cell = c0 + i;
+  if (tcnt[cell] == 0) return;
+  const Slot sl{sv + threadIdx.x};
+  float zar[P], zai[P], zbr[P], zbi[P];
+  octant_phases<P>(key[cell], zar, zai, zbr, zbi);
+  rot_pass<P, 0, 2, 3, 0>(sl, Lx + (size_t)parent[cell] * NC, nullptr, zar, zai, zbr, zbi, 1.f);
+  coax_l2l<P, 0>(sl);
+  rot_pass<P, 0, 2, 3, 2>(sl, nullptr, Lx + (size_t)cell * NC, zar, zai, zbr, zbi, 1.f);
+}
+
 // Wigner small d^n_{m'm}(b) (explicit sum)
 double wigner_d(int n, int mp, int m, double b) {
   auto fact = [](int k) {
@@ -374,6 +574,37 @@ const M2LWork& m2l_work(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, c
   FMM_CUDA(cudaStreamSynchronize(st));
   c->m2l_cache.push_back(std::move(w));
   return *c->m2l_cache.back();
+}
+
+bool m2m_rot_supported(int P) { return P == 8 || P == 10 || P == 12; }
+
+// M2M of level l (children at l + 1); scratch T must hold n_cells * NC float2
+void launch_m2m_rot(fmmbem_ctx* c, int l, const int* scnt, float2* T, cudaStream_t st) {
+  const Tree& Tr = c->tree;
+  const int ch0 = (int)Tr.lvl_off[l + 1], nch = (int)(Tr.lvl_off[l + 2] - Tr.lvl_off[l + 1]);
+  const int p0 = (int)Tr.lvl_off[l], np = (int)(Tr.lvl_off[l + 1] - Tr.lvl_off[l]);
+  switch (c->P) {
+    case 8: k_m2m_rot<8><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
+    case 10: k_m2m_rot<10><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
+    case 12: k_m2m_rot<12><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
+    default: throw Error(FMMBEM_E_INVALID, "M2M rotation not instantiated for this P");
+  }
+  k_m2m_sum<<<ceil_div((int64_t)np * c->NC, 256), 256, 0, st>>>(p0, np, c->NC, Tr.child_begin.get(),
+                                                                 Tr.child_end.get(), scnt, T, c->Mx.get());
+  FMM_CHECK_LAUNCH();
+}
+
+// L2L from level l to l + 1
+void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st) {
+  const Tree& Tr = c->tree;
+  const int ch0 = (int)Tr.lvl_off[l + 1], nch = (int)(Tr.lvl_off[l + 2] - Tr.lvl_off[l + 1]);
+  switch (c->P) {
+    case 8: k_l2l_rot<8><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
+    case 10: k_l2l_rot<10><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
+    case 12: k_l2l_rot<12><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
+    default: throw Error(FMMBEM_E_INVALID, "L2L rotation not instantiated for this P");
+  }
+  FMM_CHECK_LAUNCH();
 }
 
 void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {

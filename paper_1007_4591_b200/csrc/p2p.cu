@@ -2,8 +2,8 @@
 // contribution is obtained from directly computing the interactions between all the points
 // in the adjacent cells", "P2P ... the largest fractions").
 //
-// Work unit = one warp = one chunk of <= 32*T targets of one leaf (T targets per lane in
-// registers).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
+// Work unit = one warp = one chunk of <= 64 targets of one leaf (T = 4 targets per lane in
+// registers, so 16 lanes cover a full chunk and the two halves of the warp split the sources).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
 // and a tail chunk with few targets spreads its lanes over S source subsets (split-K, reduced in
 // shared memory) -- lanes stay busy whatever the occupancy.  The sources of the (<= 27)
 // neighbour leaves stream through a warp-private shared-memory tile, already shifted into the
@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   }
 }
 
-constexpr int P2P_T = 2;  // targets per lane
+constexpr int P2P_T = 4;      // targets per lane (register blocking: one LDS.128 feeds 4 interactions)
+constexpr int P2P_CHUNK = 64; // targets per work item (16 lanes x 4 targets x 2 source subsets)
 
 template <bool SELF, bool CHECK>
 void dispatch(const P2PArgs& a, bool pot, bool dn, int grid, cudaStream_t st) {
@@ -297,7 +298,7 @@ const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int lea
   for (auto& w : c->p2p_cache)
     if (w->tgt == &t && w->leaf_lo == leaf_lo && w->leaf_hi == leaf_hi) return *w;
   const int nl = leaf_hi - leaf_lo;
-  const int chunk = 32 * P2P_T;
+  const int chunk = P2P_CHUNK;
   cudaStream_t st = c->stream;
   auto w = std::make_unique<P2PItems>();
   w->tgt = &t;
