@@ -14,7 +14,8 @@
 // conjugate symmetric, so each real matrix X acts on the stored m >= 0 half as
 //   Re b_m' = sum_{m>=0} E_m'm Re a_m,  Im b_m' = sum_{m>0} F_m'm Im a_m,
 //   E_m'm = X_m'm + (-1)^m X_m',-m,  F_m'm = X_m'm - (-1)^m X_m',-m   (E_m'0 = X_m'0, F_m'0 = 0)
-// i.e. 2 (n+1)^2 FMAs per degree.  One thread owns one (target, source) pair; the whole pipeline
+// and since X_m',-m = (-1)^{n+m'} X_m'm for all four matrices, E = 0 when n+m+m' is odd and
+// F = 0 when it is even: (n+1)^2 FMAs per degree.  One thread owns one (target, source) pair; the whole pipeline
 // is unrolled at compile time (P is a template parameter) with the E/F tables in constant
 // memory, uniform across the warp, so they enter FFMAs as constant-bank operands.  Each thread's
 // working vector lives in a private shared-memory slot and streams through registers one degree
@@ -60,8 +61,10 @@ __device__ __forceinline__ void mat_block(const float (&ar)[n + 1], const float 
     float re = 0.f, im = 0.f;
 #pragma unroll
     for (int m = 0; m <= n; ++m) {
-      re = fmaf(c_rot[X][0][tri3(n) + mp * (n + 1) + m], ar[m], re);
-      if (m > 0) im = fmaf(c_rot[X][1][tri3(n) + mp * (n + 1) + m], ai[m], im);
+      // Wigner parity d_{m',-m}(pi/2) = (-1)^{n+m'} d_{m'm}(pi/2): E vanishes for odd n+m+m',
+      // F for even n+m+m' -- half of the products are structural zeros and are skipped here
+      if (((n + m + mp) & 1) == 0) re = fmaf(c_rot[X][0][tri3(n) + mp * (n + 1) + m], ar[m], re);
+      else if (m > 0) im = fmaf(c_rot[X][1][tri3(n) + mp * (n + 1) + m], ai[m], im);
     }
     br[mp] = re;
     bi[mp] = im;

@@ -2,8 +2,8 @@
 // contribution is obtained from directly computing the interactions between all the points
 // in the adjacent cells", "P2P ... the largest fractions").
 //
-// Work unit = one warp = one chunk of <= 64 targets of one leaf (T = 4 targets per lane in
-// registers, so 16 lanes cover a full chunk and the two halves of the warp split the sources).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
+// Work unit = one warp = one chunk of <= 64 targets of one leaf (T = 2 targets per lane in
+// registers; T = 4 with two source halves measured 2% slower).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
 // and a tail chunk with few targets spreads its lanes over S source subsets (split-K, reduced in
 // shared memory) -- lanes stay busy whatever the occupancy.  The sources of the (<= 27)
 // neighbour leaves stream through a warp-private shared-memory tile, already shifted into the
@@ -250,8 +250,8 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   }
 }
 
-constexpr int P2P_T = 4;      // targets per lane (register blocking: one LDS.128 feeds 4 interactions)
-constexpr int P2P_CHUNK = 64; // targets per work item (16 lanes x 4 targets x 2 source subsets)
+constexpr int P2P_T = 2;      // targets per lane (register blocking: one LDS.128 feeds 2 interactions)
+constexpr int P2P_CHUNK = 64; // targets per work item (32 lanes x 2 targets)
 
 template <bool SELF, bool CHECK>
 void dispatch(const P2PArgs& a, bool pot, bool dn, int grid, cudaStream_t st) {
