@@ -15,8 +15,9 @@
 //
 // Raw outputs, un-normalised potential phi = sum_j w_j / r_ij:
 //   pot = phi(x_i),   dn = n_i . grad phi(x_i) = n_i . sum_j w_j (y_j - x_i) / r^3
-// Per interaction (dn only): 3 FADD + 3 (r^2) + 1 MUFU.RSQ + 3 (w r^-3) + 3 FFMA = 12 FP32 + 1 MUFU,
-// counted as 19 flops under the SURVEY 8(d) convention.
+// Per interaction (dn only): 3 FADD + 3 (r^2) + 1 MUFU.RSQ + 3 (w r^-3) + 3 FFMA = 12 FP32 operations +
+// 1 MUFU, counted as 19 flops under the SURVEY 8(d) convention; issued as packed FP32x2 instructions
+// over the lane's two targets (6 issue slots + 1 MUFU per interaction).
 #include "kernels.cuh"
 
 namespace fmm {
@@ -46,27 +47,34 @@ struct P2PArgs {
   int* flag;
 };
 
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+
+// One source against the lane's two targets with packed FP32x2 arithmetic (FADD2/FMUL2/FFMA2 on
+// sm_100a; the scalar source coordinate is a broadcast operand): 12 packed instructions + 2 MUFU.RSQ
+// for 2 interactions.  d = s - x (source minus target), so grad phi = sum w d / r^3.
 template <bool POT, bool DN, bool MASK, bool CHECK>
-__device__ __forceinline__ void interact(const float4 s, float px, float py, float pz, float& ap, float& gx,
-                                         float& gy, float& gz, bool skip, int* flag) {
-  float dx = s.x - px, dy = s.y - py, dz = s.z - pz;
-  float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  float w = s.w;
+__device__ __forceinline__ void interact2(const float4 s, float2 px, float2 py, float2 pz, float2& ap, float2& gx,
+                                          float2& gy, float2& gz, bool skipa, bool skipb, int* flag) {
+  const float2 dx = __fadd2_rn(bc2(s.x), px), dy = __fadd2_rn(bc2(s.y), py), dz = __fadd2_rn(bc2(s.z), pz);
+  float2 r2 = __fmul2_rn(dx, dx);
+  r2 = __ffma2_rn(dy, dy, r2);
+  r2 = __ffma2_rn(dz, dz, r2);
+  float2 w = bc2(s.w);
   if (CHECK) {
-    if (r2 == 0.f) atomicOr(flag, 1);
+    if (r2.x == 0.f || r2.y == 0.f) atomicOr(flag, 1);
   }
   if (MASK) {
-    w = skip ? 0.f : w;
-    r2 = fmaxf(r2, 1e-20f);
+    w = make_float2(skipa ? 0.f : s.w, skipb ? 0.f : s.w);
+    r2 = make_float2(fmaxf(r2.x, 1e-20f), fmaxf(r2.y, 1e-20f));
   }
-  float ri = rsqrtf(r2);
-  if (POT) ap = fmaf(w, ri, ap);
+  const float2 ri = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+  if (POT) ap = __ffma2_rn(w, ri, ap);
   if (DN) {
-    float t = w * ri;
-    t *= ri * ri;
-    gx = fmaf(t, dx, gx);
-    gy = fmaf(t, dy, gy);
-    gz = fmaf(t, dz, gz);
+    float2 t = __fmul2_rn(w, ri);
+    t = __fmul2_rn(t, __fmul2_rn(ri, ri));
+    gx = __ffma2_rn(t, dx, gx);
+    gy = __ffma2_rn(t, dy, gy);
+    gz = __ffma2_rn(t, dz, gz);
   }
 }
 
@@ -133,16 +141,17 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   const int S = 32 / nl_t;                    // source subsets
   const int tl = lane % nl_t, sub = lane / nl_t;
   const bool lvalid = sub < S;
+  static_assert(T == 2, "packed FP32x2 path: two targets per lane");
   int ti[T];
-  float4 tp[T];
-  float ap[T], gx[T], gy[T], gz[T];
 #pragma unroll
   for (int k = 0; k < T; ++k) {
     const int il = tl + k * nl_t;
     ti[k] = tb + (il < nt ? il : 0);
-    tp[k] = a.tpos[ti[k]];
-    ap[k] = gx[k] = gy[k] = gz[k] = 0.f;
   }
+  const float4 ta = a.tpos[ti[0]], tb4 = a.tpos[ti[1]];
+  // negated target coordinates: s + (-x) with a broadcast source operand
+  const float2 px = make_float2(-ta.x, -tb4.x), py = make_float2(-ta.y, -tb4.y), pz = make_float2(-ta.z, -tb4.z);
+  float2 ap2 = make_float2(0.f, 0.f), gx2 = ap2, gy2 = ap2, gz2 = ap2;
   const int step = lvalid ? S : 0;
 
   for (int base = 0; base < n_src; base += TILE) {
@@ -181,33 +190,22 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
     const int mlo = SELF ? min(max(self_lo - base, 0), tcnt) : tcnt;
     const int mhi = SELF ? min(max(self_hi - base, 0), tcnt) : tcnt;
     // unmasked: [0, mlo) and [mhi, tcnt)
-#pragma unroll 2
-    for (int k = sub; k < mlo; k += step) {
-      const float4 s = tile[k];
-#pragma unroll
-      for (int q = 0; q < T; ++q)
-        interact<POT, DN, false, CHECK>(s, tp[q].x, tp[q].y, tp[q].z, ap[q], gx[q], gy[q], gz[q], false, a.flag);
-    }
+#pragma unroll 4
+    for (int k = sub; k < mlo; k += step)
+      interact2<POT, DN, false, CHECK>(tile[k], px, py, pz, ap2, gx2, gy2, gz2, false, false, a.flag);
     if (SELF) {
       int k0 = mhi + ((sub - mhi) % S + S) % S;
-#pragma unroll 2
-      for (int k = k0; k < tcnt; k += step) {
-        const float4 s = tile[k];
-#pragma unroll
-        for (int q = 0; q < T; ++q)
-          interact<POT, DN, false, CHECK>(s, tp[q].x, tp[q].y, tp[q].z, ap[q], gx[q], gy[q], gz[q], false, a.flag);
-      }
+#pragma unroll 4
+      for (int k = k0; k < tcnt; k += step)
+        interact2<POT, DN, false, CHECK>(tile[k], px, py, pz, ap2, gx2, gy2, gz2, false, false, a.flag);
       int k1 = mlo + ((sub - mlo) % S + S) % S;
       for (int k = k1; k < mhi; k += step) {
-        const float4 s = tile[k];
         const int o = own[k];
-#pragma unroll
-        for (int q = 0; q < T; ++q)
-          interact<POT, DN, true, CHECK>(s, tp[q].x, tp[q].y, tp[q].z, ap[q], gx[q], gy[q], gz[q], o == ti[q],
-                                         a.flag);
+        interact2<POT, DN, true, CHECK>(tile[k], px, py, pz, ap2, gx2, gy2, gz2, o == ti[0], o == ti[1], a.flag);
       }
     }
   }
+  float ap[T] = {ap2.x, ap2.y}, gx[T] = {gx2.x, gx2.y}, gy[T] = {gy2.x, gy2.y}, gz[T] = {gz2.x, gz2.y};
   // ---- split-K reduction over the S subsets
   if (S > 1) {
 #pragma unroll
