@@ -47,10 +47,13 @@ __host__ __device__ constexpr float factf(int n) {
 // touch the same coefficient at once -> conflict-free; the 33 stride keeps the final per-row
 // reduction conflict-free too.
 struct Slot {
-  float* base;  // &sv[0][lane]
-  __device__ __forceinline__ float& re(int c) const { return base[(2 * c) * 33]; }
-  __device__ __forceinline__ float& im(int c) const { return base[(2 * c + 1) * 33]; }
+  float2* base;  // &sv[0][lane]: (re, im) of coefficient c at base[c * 33]
+  __device__ __forceinline__ float2 get(int c) const { return base[c * 33]; }
+  __device__ __forceinline__ void set(int c, float re, float im) const { base[c * 33] = make_float2(re, im); }
+  __device__ __forceinline__ void set(int c, float2 v) const { base[c * 33] = v; }
 };
+
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
 
 // one degree block: b = X a (E/F form), a and b in registers
 template <int n, int X>
@@ -97,33 +100,23 @@ __device__ __forceinline__ void pass_a(const Slot& sl, const float2* __restrict_
   for (int m = 1; m <= n; ++m) cmul_ip(br[m], bi[m], zbr[m], zbi[m]);  // Phi(t)
   mat_block<n, 1>(br, bi, ar, ai);                    // D
 #pragma unroll
-  for (int m = 0; m <= n; ++m) {
-    sl.re(c0 + m) = ar[m] * scale;
-    sl.im(c0 + m) = ai[m] * scale;
-  }
+  for (int m = 0; m <= n; ++m) sl.set(c0 + m, __fmul2_rn(make_float2(ar[m], ai[m]), bc2(scale)));
   if constexpr (n + 1 < P) pass_a<P, n + 1>(sl, Ms, zar, zai, zbr, zbi, scale * irho, irho);
 }
 
 // coaxial translation of order column k (input scaled by rho^-n, output missing rho^-(j+1))
 template <int P, int k>
 __device__ __forceinline__ void pass_b(const Slot& sl) {
-  float tr[P - k], ti[P - k];
+  float2 t[P - k];
 #pragma unroll
-  for (int n = k; n < P; ++n) {
-    tr[n - k] = sl.re(n * (n + 1) / 2 + k);
-    ti[n - k] = sl.im(n * (n + 1) / 2 + k);
-  }
+  for (int n = k; n < P; ++n) t[n - k] = sl.get(n * (n + 1) / 2 + k);
 #pragma unroll
   for (int j = k; j < P; ++j) {
-    float re = 0.f, im = 0.f;
-#pragma unroll
-    for (int n = k; n < P; ++n) {
-      re = fmaf(factf(j + n), tr[n - k], re);
-      im = fmaf(factf(j + n), ti[n - k], im);
-    }
     const float sg = ((j + k) & 1) ? -1.f : 1.f;
-    sl.re(j * (j + 1) / 2 + k) = sg * re;
-    sl.im(j * (j + 1) / 2 + k) = sg * im;
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int n = k; n < P; ++n) acc = __ffma2_rn(bc2(sg * factf(j + n)), t[n - k], acc);  // packed re/im
+    sl.set(j * (j + 1) / 2 + k, acc);
   }
   if constexpr (k + 1 < P) pass_b<P, k + 1>(sl);
 }
@@ -136,8 +129,9 @@ __device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], co
   float ar[n + 1], ai[n + 1], br[n + 1], bi[n + 1];
 #pragma unroll
   for (int m = 0; m <= n; ++m) {
-    ar[m] = sl.re(c0 + m) * scale;
-    ai[m] = sl.im(c0 + m) * scale;
+    const float2 v = __fmul2_rn(sl.get(c0 + m), bc2(scale));
+    ar[m] = v.x;
+    ai[m] = v.y;
   }
   mat_block<n, 2>(ar, ai, br, bi);                    // D^T
 #pragma unroll
@@ -146,8 +140,7 @@ __device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], co
 #pragma unroll
   for (int m = 0; m <= n; ++m) {
     if (m > 0) cmul_ip(ar[m], ai[m], zar[m], -zai[m]);  // Phi(-p - pi/2)
-    sl.re(c0 + m) = ar[m];
-    sl.im(c0 + m) = ai[m];
+    sl.set(c0 + m, ar[m], ai[m]);
   }
   if constexpr (n + 1 < P) pass_c<P, n + 1>(sl, zar, zai, zbr, zbi, scale * irho, irho);
 }
@@ -160,10 +153,10 @@ __global__ void __launch_bounds__(32 * W) k_m2l_rot(int rows, const int* __restr
                                                     float2* __restrict__ Lx) {
   constexpr int NC = P * (P + 1) / 2;
   constexpr int NR = (NC + 31) / 32;
-  __shared__ float svall[W][2 * NC * 33];
+  __shared__ float2 svall[W][NC * 33];
   const int row = blockIdx.x * W + (threadIdx.x >> 5);
   if (row >= rows) return;
-  float* sv = svall[threadIdx.x >> 5];
+  float2* sv = svall[threadIdx.x >> 5];
   const int cell = tcells[row];
   const int lo = off[row], hi = off[row + 1];
   const int lane = threadIdx.x & 31;
@@ -207,24 +200,17 @@ __global__ void __launch_bounds__(32 * W) k_m2l_rot(int rows, const int* __restr
       pass_c<P, 0>(sl, zar, zai, zbr, zbi, irho, irho);
     } else {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        sl.re(c) = 0.f;
-        sl.im(c) = 0.f;
-      }
+      for (int c = 0; c < NC; ++c) sl.set(c, 0.f, 0.f);
     }
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const int c = lane + 32 * r;
       if (c < NC) {
-        float sx = 0.f, sy = 0.f;
+        float2 sum = make_float2(0.f, 0.f);
 #pragma unroll 8
-        for (int l = 0; l < 32; ++l) {
-          sx += sv[(2 * c) * 33 + l];
-          sy += sv[(2 * c + 1) * 33 + l];
-        }
-        acc[r].x += sx;
-        acc[r].y += sy;
+        for (int l = 0; l < 32; ++l) sum = __fadd2_rn(sum, sv[c * 33 + l]);
+        acc[r] = __fadd2_rn(acc[r], sum);
       }
     }
     __syncwarp();
@@ -282,17 +268,15 @@ __device__ __forceinline__ void rot_pass(const Slot& sl, const float2* __restric
       ar[m] = q.x;
       ai[m] = q.y;
     } else {
-      ar[m] = sl.re(c0 + m);
-      ai[m] = sl.im(c0 + m);
+      const float2 v = sl.get(c0 + m);
+      ar[m] = v.x;
+      ai[m] = v.y;
     }
   }
   if (MODE == 0) {
     rot_block<n, XA, XB>(ar, ai, zar, zai, zbr, zbi, 1.f, 1.f);
 #pragma unroll
-    for (int m = 0; m <= n; ++m) {
-      sl.re(c0 + m) = ar[m];
-      sl.im(c0 + m) = ai[m];
-    }
+    for (int m = 0; m <= n; ++m) sl.set(c0 + m, ar[m], ai[m]);
   } else {
     // back rotation: XB Phi(-t) XA, then Phi(-p - pi/2)
     float br[n + 1], bi[n + 1];
@@ -318,24 +302,16 @@ __device__ __forceinline__ void rot_pass(const Slot& sl, const float2* __restric
 // coaxial M2M along +z by RHO8: M_n^k <- sum_{j=k}^{n} 2^-j M_j^k rho^(n-j)/(n-j)!
 template <int P, int k>
 __device__ __forceinline__ void coax_m2m(const Slot& sl) {
-  float tr[P - k], ti[P - k];
+  float2 t[P - k];
 #pragma unroll
-  for (int j = k; j < P; ++j) {
-    tr[j - k] = sl.re(j * (j + 1) / 2 + k);
-    ti[j - k] = sl.im(j * (j + 1) / 2 + k);
-  }
+  for (int j = k; j < P; ++j) t[j - k] = sl.get(j * (j + 1) / 2 + k);
 #pragma unroll
   for (int n = k; n < P; ++n) {
-    float re = 0.f, im = 0.f;
+    float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int j = k; j <= n; ++j) {
-      constexpr float one = 1.f;
-      const float cf = one / powf_c(2.f, j) * powf_c(RHO8, n - j) / factf(n - j);
-      re = fmaf(cf, tr[j - k], re);
-      im = fmaf(cf, ti[j - k], im);
-    }
-    sl.re(n * (n + 1) / 2 + k) = re;
-    sl.im(n * (n + 1) / 2 + k) = im;
+    for (int j = k; j <= n; ++j)
+      acc = __ffma2_rn(bc2(1.f / powf_c(2.f, j) * powf_c(RHO8, n - j) / factf(n - j)), t[j - k], acc);
+    sl.set(n * (n + 1) / 2 + k, acc);
   }
   if constexpr (k + 1 < P) coax_m2m<P, k + 1>(sl);
 }
@@ -343,23 +319,16 @@ __device__ __forceinline__ void coax_m2m(const Slot& sl) {
 // coaxial L2L along +z by RHO8: L_j^k <- 2^-(j+1) sum_{n=j}^{P-1} L_n^k rho^(n-j)/(n-j)!
 template <int P, int k>
 __device__ __forceinline__ void coax_l2l(const Slot& sl) {
-  float tr[P - k], ti[P - k];
+  float2 t[P - k];
 #pragma unroll
-  for (int n = k; n < P; ++n) {
-    tr[n - k] = sl.re(n * (n + 1) / 2 + k);
-    ti[n - k] = sl.im(n * (n + 1) / 2 + k);
-  }
+  for (int n = k; n < P; ++n) t[n - k] = sl.get(n * (n + 1) / 2 + k);
 #pragma unroll
   for (int j = k; j < P; ++j) {
-    float re = 0.f, im = 0.f;
+    float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int n = j; n < P; ++n) {
-      const float cf = 1.f / powf_c(2.f, j + 1) * powf_c(RHO8, n - j) / factf(n - j);
-      re = fmaf(cf, tr[n - k], re);
-      im = fmaf(cf, ti[n - k], im);
-    }
-    sl.re(j * (j + 1) / 2 + k) = re;
-    sl.im(j * (j + 1) / 2 + k) = im;
+    for (int n = j; n < P; ++n)
+      acc = __ffma2_rn(bc2(1.f / powf_c(2.f, j + 1) * powf_c(RHO8, n - j) / factf(n - j)), t[n - k], acc);
+    sl.set(j * (j + 1) / 2 + k, acc);
   }
   if constexpr (k + 1 < P) coax_l2l<P, k + 1>(sl);
 }
@@ -391,7 +360,7 @@ __global__ void __launch_bounds__(32) k_m2m_rot(int c0, int n, const uint64_t* _
                                                 const int* __restrict__ scnt, const float2* __restrict__ M,
                                                 float2* __restrict__ T) {
   constexpr int NC = P * (P + 1) / 2;
-  __shared__ float sv[2 * NC * 33];
+  __shared__ float2 sv[NC * 33];
   const int i = blockIdx.x * 32 + threadIdx.x;
   if (i >= n) return;
   const int cell = c0 + i;
@@ -428,7 +397,7 @@ __global__ void __launch_bounds__(32) k_l2l_rot(int c0, int n, const uint64_t* _
                                                 const int* __restrict__ parent, const int* __restrict__ tcnt,
                                                 float2* __restrict__ Lx) {
   constexpr int NC = P * (P + 1) / 2;
-  __shared__ float sv[2 * NC * 33];
+  __shared__ float2 sv[NC * 33];
   const int i = blockIdx.x * 32 + threadIdx.x;
   if (i >= n) return;
   const int cell = c0 + i;
