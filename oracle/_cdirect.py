@@ -36,6 +36,8 @@ def lib():
         L.oracle_pot_sum.argtypes = [ctypes.c_int64, d, i, ctypes.c_int64, d, d, i, d]
         L.oracle_pot_sum.restype = ctypes.c_int
         L.oracle_threads.restype = ctypes.c_int
+        L.oracle_tri_integrals.argtypes = [ctypes.c_int64, d, d, d, ctypes.POINTER(ctypes.c_int32), d, d]
+        L.oracle_tri_integrals.restype = None
         _lib = L
     return _lib
 
@@ -76,3 +78,16 @@ def pot_sum(x, tid, y, w, owner):
     if bad:
         raise ValueError("coincident target/source pair (SURVEY A14)")
     return out
+
+
+def tri_integrals(x, n, tv, self_flags=None):
+    """Per row k: (int_T G(x_k, y) dA, int_T dG/dn_x(x_k, y) dA) over triangle tv[k] (3x3)."""
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    n = np.ascontiguousarray(n, np.float64).reshape(-1, 3)
+    tv = np.ascontiguousarray(tv, np.float64).reshape(-1, 9)
+    sf = None if self_flags is None else np.ascontiguousarray(self_flags, np.int32)
+    pot, dn = np.zeros(len(x)), np.zeros(len(x))
+    lib().oracle_tri_integrals(len(x), _dp(x), _dp(n), _dp(tv),
+                               None if sf is None else sf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                               _dp(pot), _dp(dn))
+    return pot, dn

@@ -65,6 +65,7 @@ class Panels:
         if t.size and (t.min() < 0 or t.max() >= len(v)):
             raise ValueError("triangle index out of range")
         v0, v1, v2 = v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
+        self.tri_v = np.stack([v0, v1, v2], 1)  # [n, 3 vertices, 3]
         cr = np.cross(v1 - v0, v2 - v0)
         nrm = np.linalg.norm(cr, axis=1)
         scale2 = float(np.sum((v.max(0) - v.min(0)) ** 2)) if len(v) else 1.0
@@ -118,6 +119,56 @@ def apply_single(pan: Panels, x, rows=None):
     w = np.repeat(np.asarray(x, np.float64), pan.K) * aw
     idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)
     return _cdirect.pot_sum(pan.centroid[idx], idx, y, w, owner)
+
+
+def near_pairs(pan: Panels, eta: float):
+    """Near pairs of the analytic option: j != i with |c_i - c_j| < eta sqrt(A_j)."""
+    from scipy.spatial import cKDTree
+    rmax = eta * np.sqrt(pan.area.max())
+    pr = cKDTree(pan.centroid).query_pairs(rmax, output_type="ndarray")
+    if len(pr) == 0:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64)
+    both = np.concatenate([pr, pr[:, ::-1]])
+    i, j = both[:, 0].astype(np.int64), both[:, 1].astype(np.int64)
+    keep = np.linalg.norm(pan.centroid[i] - pan.centroid[j], axis=1) < eta * np.sqrt(pan.area[j])
+    o = np.lexsort((j[keep], i[keep]))
+    return i[keep][o], j[keep][o]
+
+
+def near_corrections(pan: Panels, eta: float):
+    """For near_mode = 1: per near pair, (exact panel integral) - (K-point quadrature) of
+    G and of dG/dn_i, and the single-layer self integrals int_{T_i} G(c_i, y) dA.  The exact
+    integrals are done numerically (oracle/direct.c: adaptive subdivision / Duffy), never by the
+    closed forms the CUDA path uses."""
+    key = ("near", eta)
+    if key in pan.__dict__:
+        return pan.__dict__[key]
+    i, j = near_pairs(pan, eta)
+    ex_pot, ex_dn = _cdirect.tri_integrals(pan.centroid[i], pan.normal[i], pan.tri_v[j])
+    q_pot, q_dn = np.zeros(len(i)), np.zeros(len(i))
+    for g in range(pan.K):
+        d = pan.centroid[i] - pan.qpts[j, g, :]
+        r = np.linalg.norm(d, axis=1)
+        q_pot += pan.wq[g] * pan.area[j] / (4 * np.pi * r)
+        q_dn += pan.wq[g] * pan.area[j] * (-np.einsum("ij,ij->i", pan.normal[i], d) / (4 * np.pi * r ** 3))
+    self_pot, _ = _cdirect.tri_integrals(pan.centroid, pan.normal, pan.tri_v, np.ones(pan.n, np.int32))
+    out = (i, j, ex_pot - q_pot, ex_dn - q_dn, self_pot)
+    pan.__dict__[key] = out
+    return out
+
+
+def apply_kprime_near(pan: Panels, x, eta: float = 3.0):
+    """O4 with near_mode = 1: K' with the exact flat-panel integral for the near pairs."""
+    i, j, _, c_dn, _ = near_corrections(pan, eta)
+    x = np.asarray(x, np.float64)
+    return apply_kprime(pan, x) + np.bincount(i, weights=c_dn * x[j], minlength=pan.n)
+
+
+def apply_single_near(pan: Panels, x, eta: float = 3.0):
+    """O5 with near_mode = 1: V with exact near-pair integrals and the analytic self term (A7)."""
+    i, j, c_pot, _, self_pot = near_corrections(pan, eta)
+    x = np.asarray(x, np.float64)
+    return apply_single(pan, x) + np.bincount(i, weights=c_pot * x[j], minlength=pan.n) + self_pot * x
 
 
 def apply_A(pan: Panels, x, f: float):

@@ -311,3 +311,55 @@ def test_binding_decoupling():
 def test_rel_l2():
     assert bem.rel_l2([1.0, 2.0], [1.0, 2.0]) == 0.0
     assert bem.rel_l2([2.0, 0.0], [1.0, 0.0]) == pytest.approx(1.0)
+
+
+# ---------------------------------------------------------------- near-field option (a11)
+def test_triangle_integrals_match_scipy_dblquad():
+    """The oracle's panel integrals (adaptive subdivision / Duffy) equal scipy's dblquad over the
+    triangle's parameter domain (an independent library integrator)."""
+    from scipy.integrate import dblquad
+    tv = np.array([[0.0, 0, 0], [1.0, 0.1, 0], [0.2, 0.9, 0.1]])
+    n = np.array([0.3, -0.2, 0.9]); n /= np.linalg.norm(n)
+    J = np.linalg.norm(np.cross(tv[1] - tv[0], tv[2] - tv[0]))
+    for x in (np.array([0.3, 0.3, 0.4]), np.array([1.3, 1.1, 0.05]), np.array([0.45, 0.35, -0.02])):
+        def y(u, v):
+            return tv[0] + u * (tv[1] - tv[0]) + v * (tv[2] - tv[0])
+        gp = dblquad(lambda v, u: J / (4 * np.pi * np.linalg.norm(x - y(u, v))), 0, 1, 0, lambda u: 1 - u,
+                     epsabs=1e-13, epsrel=1e-11)[0]
+        gd = dblquad(lambda v, u: J * (-(n @ (x - y(u, v))) / (4 * np.pi * np.linalg.norm(x - y(u, v)) ** 3)),
+                     0, 1, 0, lambda u: 1 - u, epsabs=1e-13, epsrel=1e-11)[0]
+        pot, dn = _cdirect.tri_integrals(x[None], n[None], tv.reshape(1, 9))
+        assert pot[0] == pytest.approx(gp, rel=1e-8)
+        assert dn[0] == pytest.approx(gd, rel=1e-7, abs=1e-12)
+
+
+def test_triangle_integrals_limits():
+    """Far away the panel integral tends to A G(x, c) with an O((h/d)^2) error; the self integral
+    of an equilateral triangle at its centroid equals 3 * (side/(4 pi)) * asinh(sqrt 3) / sqrt 3 * ...
+    closed form int 1/r = 3 h ln((1+sin 60)/cos 60)... checked against Duffy on subdivided copies."""
+    tv = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.5, np.sqrt(3) / 2, 0]])
+    c = tv.mean(0); A = np.sqrt(3) / 4
+    errs = []
+    for d in (4.0, 8.0, 16.0):
+        x = c + np.array([0.3, 0.2, 1.0]) / np.linalg.norm([0.3, 0.2, 1.0]) * d
+        pot, _ = _cdirect.tri_integrals(x[None], np.array([[0, 0, 1.0]]), tv.reshape(1, 9))
+        errs.append(abs(pot[0] / (A / (4 * np.pi * d)) - 1))
+    assert errs[0] / errs[1] == pytest.approx(4.0, rel=0.1) and errs[1] / errs[2] == pytest.approx(4.0, rel=0.1)
+    # centroid of an equilateral triangle of side s: int_T dA/r = 3 * r_in * ln((1 + sin 60)/(1 - sin 60))
+    # ... with r_in = s / (2 sqrt 3) the inradius (sum over the 3 edges of the in-plane line integral)
+    r_in = 1.0 / (2 * np.sqrt(3))
+    exact = 3 * r_in * np.log((1 + np.sin(np.pi / 3)) / (1 - np.sin(np.pi / 3))) / (4 * np.pi)
+    pot, dn = _cdirect.tri_integrals(c[None], np.array([[0, 0, 1.0]]), tv.reshape(1, 9), np.ones(1, np.int32))
+    assert pot[0] == pytest.approx(exact, rel=1e-12) and dn[0] == 0.0
+
+
+def test_near_operator_consistency():
+    """Near correction: exact - quadrature is small for the farther pairs and the corrected K'
+    still has the sphere eigenvalue -1/2 for the constant."""
+    p = bem.Panels(*octasphere(12))
+    i, j, c_pot, c_dn, self_pot = bem.near_corrections(p, 3.0)
+    assert len(i) > 0 and np.all(i != j)
+    x = np.ones(p.n)
+    assert abs(np.mean(bem.apply_kprime_near(p, x)) + 0.5) < 0.03
+    # the single-layer self term of a flat panel is positive and O(sqrt(A))
+    assert np.all(self_pot > 0) and np.allclose(self_pot / np.sqrt(p.area), self_pot[0] / np.sqrt(p.area[0]), rtol=0.3)
