@@ -66,8 +66,10 @@ typedef struct {
   int32_t terms;         /* P = number of expansion terms, degrees 0..P-1 (A9); 2..16, default 10 */
   int32_t leaf_points;   /* depth rule: mean panels per occupied leaf <= leaf_points (A10); default 64 */
   int32_t quad_points;   /* K in {1 (paper), 3, 6, 7}; default 1 */
-  int32_t near_mode;     /* 0 only (analytic near field is a later row); default 0 */
-  float near_radius;     /* reserved */
+  int32_t near_mode;     /* 0 = K-point quadrature only (paper); 1 = exact flat-panel integrals (closed form,
+                            P:415-418) for pairs |c_i - c_j| < near_radius*sqrt(A_j) and the single-layer
+                            self term; default 0 */
+  float near_radius;     /* eta of the near criterion; default 3; eta*sqrt(A) must stay below the leaf width */
   int32_t self_term;     /* 0 only: K'_ii = 0 (flat panel) */
   int32_t direct;        /* 1 = bypass the FMM: all-pairs P2P (paper Fig. 11 "direct") */
   int32_t deterministic; /* reductions have a fixed order (no atomics on results); always true */

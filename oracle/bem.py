@@ -284,8 +284,9 @@ BIBEE_SCALE = {"cfa": -0.5, "p": 0.0, "lb": 0.5}
 class Problem:
     """A molecule: mesh + charges + dielectrics; the full oracle pipeline (O1-O9)."""
 
-    def __init__(self, cfg, K: int = 1):
+    def __init__(self, cfg, K: int = 1, near_eta=None):
         self.pan = Panels(cfg["vertices"], cfg["triangles"], K)
+        self.near_eta = near_eta  # None: paper's quadrature only; else the analytic near-field option
         self.cxyz = np.asarray(cfg["charge_xyz"], np.float64).reshape(-1, 3)
         self.cq = np.asarray(cfg["charge_q"], np.float64).reshape(-1)
         self.eps_in, self.eps_out = float(cfg["eps_in"]), float(cfg["eps_out"])
@@ -306,8 +307,11 @@ class Problem:
             sigma = solve_dense(self.pan, self.E, self.f)
             info = dict(iterations=0, converged=True)
         else:
-            sigma, its, hist, conv = gmres(lambda v: apply_A(self.pan, v, self.f), self.f * self.E,
-                                           tol, restart, max_iters)
+            if self.near_eta is None:
+                op = lambda v: apply_A(self.pan, v, self.f)  # noqa: E731
+            else:
+                op = lambda v: np.asarray(v) - self.f * apply_kprime_near(self.pan, v, self.near_eta)  # noqa: E731
+            sigma, its, hist, conv = gmres(op, self.f * self.E, tol, restart, max_iters)
             info = dict(iterations=its, converged=conv, history=hist)
         e, kcal = self.energy_of(sigma)
         return dict(sigma=sigma, dG=e, dG_kcal=kcal, **info)

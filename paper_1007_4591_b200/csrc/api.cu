@@ -235,6 +235,12 @@ void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_
   if (timing) cudaEventRecord(c->ev[7], st);
   SrcArg s = kp_src(c, x, st, &dist);
   fmm_eval(c, t, s, o, /*self=*/true, /*check=*/false, st, timing, dist);
+  if (c->opt.near_mode) {  // analytic near-field correction (a11): y += b C x over full x
+    const bool single = (op == FMMBEM_OP_SINGLE);
+    const float b = (op == FMMBEM_OP_A) ? (float)(-c->f) : 1.f;
+    apply_near(c, single, s.x, yg, b, st);
+  }
+  if (timing) cudaEventRecord(c->ev[9], st);
 }
 
 void apply_A(fmmbem_ctx* c, const float* x, float* y, cudaStream_t s) { apply_op(c, FMMBEM_OP_A, x, y, s, false); }
@@ -358,6 +364,11 @@ void fill_timing(fmmbem_ctx* c, bool direct) {
   T.p2p = t[2];
   T.l2p = t[3] + (t[1] - tm);
   T.total += t[0] + t[1] + t[2] + t[3];
+  float tn = 0;
+  if (cudaEventElapsedTime(&tn, c->ev[4], c->ev[9]) == cudaSuccess) {
+    T.near = tn;
+    T.total += tn;
+  }
   T.p2p_interactions = c->p2p_inter_kp;
   T.m2l_pairs = direct ? 0 : c->m2l_pairs_kp;
 }
@@ -417,7 +428,8 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   if (opt.leaf_points < 1) throw Error(FMMBEM_E_INVALID, "leaf_points must be >= 1");
   if (!(opt.quad_points == 1 || opt.quad_points == 3 || opt.quad_points == 6 || opt.quad_points == 7))
     throw Error(FMMBEM_E_INVALID, "quad_points must be 1, 3, 6 or 7");
-  if (opt.near_mode != 0) throw Error(FMMBEM_E_INVALID, "near_mode = 1 (analytic near field) is not available yet");
+  if (opt.near_mode != 0 && opt.near_mode != 1) throw Error(FMMBEM_E_INVALID, "near_mode must be 0 or 1");
+  if (opt.near_mode == 1 && !(opt.near_radius > 0.f)) throw Error(FMMBEM_E_INVALID, "near_radius must be > 0");
   if (opt.self_term != 0) throw Error(FMMBEM_E_INVALID, "self_term = 1 is not available yet");
   if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks) throw Error(FMMBEM_E_INVALID, "bad rank / nranks");
   if (opt.nranks > 1 && !opt.nccl_id) throw Error(FMMBEM_E_INVALID, "nranks > 1 needs options.nccl_id");
@@ -496,8 +508,6 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
     throw Error(FMMBEM_E_DEGENERATE, std::string(range ? "triangle index out of range" : "degenerate triangle") +
                                          " " + std::to_string(bad));
   }
-  dV.release();
-  dT.release();
   if (nc) {
     cx.alloc(3 * nc);
     cq.alloc(nc);
@@ -522,6 +532,9 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
     comm_init(c, opt.nccl_id);
     partition(c, s);
   }
+  if (c->opt.near_mode == 1) build_near(c, dV.get(), dT.get(), cen.get(), nrm.get(), area.get(), beta.get(), wq.get(), s);
+  dV.release();
+  dT.release();
   c->m2l_pairs_kp = 0;
   if (!(c->opt.direct != 0 || c->tree.L < 2)) {
     const int* tc = (c->nranks > 1) ? c->pan_own_cnt.get() : c->pan.cell_cnt.get();

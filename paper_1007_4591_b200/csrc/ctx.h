@@ -55,6 +55,13 @@ struct P2PItems {
   DevBuf<int4> items;
 };
 
+// analytic near-field correction (near_mode = 1): CSR over this rank's target rows
+struct NearCSR {
+  int64_t nnz = 0;
+  DevBuf<int> off, col;
+  DevBuf<float> vkp, vsl, diag;
+};
+
 struct Timing {
   cudaEvent_t ev[12];
   bool valid = false;
@@ -106,6 +113,7 @@ struct fmmbem_ctx {
   std::vector<int64_t> pan_offs;
   fmm::DevBuf<int> pan_own_cnt, quad_own_cnt;  // subtree counts of owned points
   fmm::DevBuf<float> xfull;                    // all-gathered source weights
+  fmm::NearCSR near;                           // near_mode = 1 corrections
   int64_t n_own() const { return pan_hi - pan_lo; }
   fmmbem_timing last{};
   cudaEvent_t ev[10] = {};

@@ -45,6 +45,11 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
                 bool direct, cudaStream_t st);
 const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi);
 
+// analytic near field (near.cu)
+void build_near(fmmbem_ctx* c, const double* V, const int* T, const double* cen, const double* nrm,
+                const double* area, const double* beta, const double* wq, cudaStream_t st);
+void apply_near(fmmbem_ctx* c, bool single, const float* x_full, float* y_global, float b, cudaStream_t st);
+
 // multi-GPU (comm.cu); all no-ops when nranks == 1
 void comm_unique_id(void* id128);
 void comm_init(fmmbem_ctx* c, const void* id128);

@@ -212,3 +212,31 @@ def test_rotation_m2l_equals_plain_translation(problems, monkeypatch, terms):
         monkeypatch.setenv("FMMBEM_M2L", mode)
         ys[mode] = run(solver(cfg, terms=terms, leaf_points=16), x, "kprime")
     assert bem.rel_l2(ys["rot"], ys["p4"]) < 2e-6
+
+
+@pytest.mark.parametrize("op", ["kprime", "single", "A"])
+def test_near_mode_matches_oracle(problems, op):
+    """near_mode = 1 (a11): closed-form flat-panel integrals on the GPU vs the oracle's adaptive /
+    Duffy quadrature of the same integrals, through the whole operator."""
+    cfg, P = problems["lyso20"]
+    x = np.random.default_rng(9).normal(size=P.pan.n)
+    if op == "kprime":
+        ref = bem.apply_kprime_near(P.pan, x, 3.0)
+    elif op == "single":
+        ref = bem.apply_single_near(P.pan, x, 3.0)
+    else:
+        ref = x - P.f * bem.apply_kprime_near(P.pan, x, 3.0)
+    plain = ref_op(P, x, op)
+    assert bem.rel_l2(ref, plain) > 1e-4  # the correction is visible at this tolerance
+    for direct, tol in ((1, 2e-5), (0, 1e-4)):
+        s = solver(cfg, near_mode=1, near_radius=3.0, direct=direct, terms=12, leaf_points=16)
+        err = bem.rel_l2(run(s, x, op), ref)
+        assert err < tol, (direct, err)
+
+
+def test_near_mode_solve_energy():
+    cfg = configs.lysozyme(nu=20, n_atoms=200)
+    s = solver(cfg, near_mode=1, terms=12, leaf_points=16)
+    r = s.solve()
+    ref = bem.Problem(cfg, near_eta=3.0).solve("gmres")
+    assert abs(r["dG"] / ref["dG"] - 1) < 1e-3, (r["dG"], ref["dG"])
