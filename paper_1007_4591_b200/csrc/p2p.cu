@@ -141,17 +141,24 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   const int S = 32 / nl_t;                    // source subsets
   const int tl = lane % nl_t, sub = lane / nl_t;
   const bool lvalid = sub < S;
-  static_assert(T == 2, "packed FP32x2 path: two targets per lane");
+  static_assert(T % 2 == 0, "packed FP32x2 path: pairs of targets per lane");
+  constexpr int NP = T / 2;
   int ti[T];
 #pragma unroll
   for (int k = 0; k < T; ++k) {
     const int il = tl + k * nl_t;
     ti[k] = tb + (il < nt ? il : 0);
   }
-  const float4 ta = a.tpos[ti[0]], tb4 = a.tpos[ti[1]];
-  // negated target coordinates: s + (-x) with a broadcast source operand
-  const float2 px = make_float2(-ta.x, -tb4.x), py = make_float2(-ta.y, -tb4.y), pz = make_float2(-ta.z, -tb4.z);
-  float2 ap2 = make_float2(0.f, 0.f), gx2 = ap2, gy2 = ap2, gz2 = ap2;
+  // negated target coordinates of each packed pair: s + (-x) with a broadcast source operand
+  float2 px[NP], py[NP], pz[NP], ap2[NP], gx2[NP], gy2[NP], gz2[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const float4 ta = a.tpos[ti[2 * q]], tb4 = a.tpos[ti[2 * q + 1]];
+    px[q] = make_float2(-ta.x, -tb4.x);
+    py[q] = make_float2(-ta.y, -tb4.y);
+    pz[q] = make_float2(-ta.z, -tb4.z);
+    ap2[q] = gx2[q] = gy2[q] = gz2[q] = make_float2(0.f, 0.f);
+  }
   const int step = lvalid ? S : 0;
 
   for (int base = 0; base < n_src; base += TILE) {
@@ -191,21 +198,42 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
     const int mhi = SELF ? min(max(self_hi - base, 0), tcnt) : tcnt;
     // unmasked: [0, mlo) and [mhi, tcnt)
 #pragma unroll 4
-    for (int k = sub; k < mlo; k += step)
-      interact2<POT, DN, false, CHECK>(tile[k], px, py, pz, ap2, gx2, gy2, gz2, false, false, a.flag);
+    for (int k = sub; k < mlo; k += step) {
+      const float4 sv = tile[k];
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+        interact2<POT, DN, false, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], false, false,
+                                         a.flag);
+    }
     if (SELF) {
       int k0 = mhi + ((sub - mhi) % S + S) % S;
 #pragma unroll 4
-      for (int k = k0; k < tcnt; k += step)
-        interact2<POT, DN, false, CHECK>(tile[k], px, py, pz, ap2, gx2, gy2, gz2, false, false, a.flag);
+      for (int k = k0; k < tcnt; k += step) {
+        const float4 sv = tile[k];
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+          interact2<POT, DN, false, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], false, false,
+                                           a.flag);
+      }
       int k1 = mlo + ((sub - mlo) % S + S) % S;
       for (int k = k1; k < mhi; k += step) {
         const int o = own[k];
-        interact2<POT, DN, true, CHECK>(tile[k], px, py, pz, ap2, gx2, gy2, gz2, o == ti[0], o == ti[1], a.flag);
+        const float4 sv = tile[k];
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+          interact2<POT, DN, true, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], o == ti[2 * q],
+                                          o == ti[2 * q + 1], a.flag);
       }
     }
   }
-  float ap[T] = {ap2.x, ap2.y}, gx[T] = {gx2.x, gx2.y}, gy[T] = {gy2.x, gy2.y}, gz[T] = {gz2.x, gz2.y};
+  float ap[T], gx[T], gy[T], gz[T];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    ap[2 * q] = ap2[q].x; ap[2 * q + 1] = ap2[q].y;
+    gx[2 * q] = gx2[q].x; gx[2 * q + 1] = gx2[q].y;
+    gy[2 * q] = gy2[q].x; gy[2 * q + 1] = gy2[q].y;
+    gz[2 * q] = gz2[q].x; gz[2 * q + 1] = gz2[q].y;
+  }
   // ---- split-K reduction over the S subsets
   if (S > 1) {
 #pragma unroll
@@ -248,8 +276,8 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   }
 }
 
-constexpr int P2P_T = 2;      // targets per lane (register blocking: one LDS.128 feeds 2 interactions)
-constexpr int P2P_CHUNK = 64; // targets per work item (32 lanes x 2 targets)
+constexpr int P2P_T = 4;      // targets per lane: two packed FP32x2 pairs per shared-memory source load
+constexpr int P2P_CHUNK = 64; // targets per work item (16 lanes x 4 targets x 2 source halves)
 
 template <bool SELF, bool CHECK>
 void dispatch(const P2PArgs& a, bool pot, bool dn, int grid, cudaStream_t st) {

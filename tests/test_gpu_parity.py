@@ -229,14 +229,14 @@ def test_near_mode_matches_oracle(problems, op):
     plain = ref_op(P, x, op)
     assert bem.rel_l2(ref, plain) > 1e-4  # the correction is visible at this tolerance
     for direct, tol in ((1, 2e-5), (0, 1e-4)):
-        s = solver(cfg, near_mode=1, near_radius=3.0, direct=direct, terms=12, leaf_points=16)
+        s = solver(cfg, near_mode=1, near_radius=3.0, direct=direct, terms=12, leaf_points=64)
         err = bem.rel_l2(run(s, x, op), ref)
         assert err < tol, (direct, err)
 
 
 def test_near_mode_solve_energy():
     cfg = configs.lysozyme(nu=20, n_atoms=200)
-    s = solver(cfg, near_mode=1, terms=12, leaf_points=16)
+    s = solver(cfg, near_mode=1, terms=12, leaf_points=64)
     r = s.solve()
     ref = bem.Problem(cfg, near_eta=3.0).solve("gmres")
     assert abs(r["dG"] / ref["dG"] - 1) < 1e-3, (r["dG"], ref["dG"])
