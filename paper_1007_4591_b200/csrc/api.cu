@@ -176,38 +176,63 @@ TgtArg own_targets(fmmbem_ctx* c, bool quad) {
 
 }  // namespace
 
+enum : int {
+  E_START = 0, E_UP0, E_UP1, E_AR0, E_AR1, E_M2L0, E_M2L1, E_DN1, E_P2P0, E_P2P1, E_L2P0, E_L2P1, E_AG0, E_AG1,
+  E_NEAR1, E_END
+};
+
+// One FMM (or direct) evaluation.  With c->overlap the near field (P2P, independent of every
+// expansion) runs on a side stream concurrently with the upward sweep, the multipole exchange and
+// M2L/L2L; L2P then waits for it (y is first written by P2P, L2P accumulates).
 void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
               cudaStream_t st, bool timing, bool distributed) {
   const bool direct = c->opt.direct != 0 || c->tree.L < 2;
-  if (timing) cudaEventRecord(c->ev[0], st);
+  auto rec = [&](int e, cudaStream_t q) {
+    if (timing) cudaEventRecord(c->ev[e], q);
+  };
+  rec(E_START, st);
+  const bool ovl = c->overlap && !direct;
+  cudaStream_t ps = ovl ? c->side : st;
+  if (ovl) {
+    FMM_CUDA(cudaEventRecord(c->fork, st));
+    FMM_CUDA(cudaStreamWaitEvent(ps, c->fork, 0));
+    rec(E_P2P0, ps);
+    launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, ps);
+    rec(E_P2P1, ps);
+    FMM_CUDA(cudaEventRecord(c->join, ps));
+  }
   if (!direct) {
+    rec(E_UP0, st);
     launch_upward(c, s, st);
+    rec(E_UP1, st);
     if (distributed) {  // partial multipoles of the owned subtrees -> every cell's full multipole
-      if (timing) cudaEventRecord(c->ev[5], st);
+      rec(E_AR0, st);
       const size_t off = (size_t)c->tree.lvl_off[2] * c->NC;
       comm_allreduce_f32(c, reinterpret_cast<float*>(c->Mx.get() + off), 2 * (c->Mx.n - off), st);
-      if (timing) cudaEventRecord(c->ev[6], st);
+      rec(E_AR1, st);
     }
-    if (timing) cudaEventRecord(c->ev[1], st);
     const int* tcnt = t.cnt ? t.cnt : t.set->cell_cnt.get();
+    rec(E_M2L0, st);
     launch_m2l(c, s.set->cell_cnt.get(), tcnt, st);
-    if (timing) cudaEventRecord(c->ev[8], st);
+    rec(E_M2L1, st);
     launch_downward(c, tcnt, st);
-    if (timing) cudaEventRecord(c->ev[2], st);
-  } else if (timing) {
-    cudaEventRecord(c->ev[1], st);
-    cudaEventRecord(c->ev[8], st);
-    cudaEventRecord(c->ev[2], st);
+    rec(E_DN1, st);
   }
-  launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
-  if (timing) cudaEventRecord(c->ev[3], st);
+  if (!ovl) {
+    rec(E_P2P0, st);
+    launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
+    rec(E_P2P1, st);
+  } else {
+    FMM_CUDA(cudaStreamWaitEvent(st, c->join, 0));
+  }
+  rec(E_L2P0, st);
   if (!direct) {
     Outputs acc = o;
     acc.pot.x = nullptr;
     acc.dn.x = nullptr;
     launch_l2p(c, t, acc, st);
   }
-  if (timing) cudaEventRecord(c->ev[4], st);
+  rec(E_L2P1, st);
   c->timed_comm = timing && distributed && !direct;
 }
 
@@ -232,15 +257,17 @@ void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_
     }
   }
   bool dist = false;
-  if (timing) cudaEventRecord(c->ev[7], st);
+  if (timing) cudaEventRecord(c->ev[E_AG0], st);
   SrcArg s = kp_src(c, x, st, &dist);
+  if (timing) cudaEventRecord(c->ev[E_AG1], st);
   fmm_eval(c, t, s, o, /*self=*/true, /*check=*/false, st, timing, dist);
   if (c->opt.near_mode) {  // analytic near-field correction (a11): y += b C x over full x
     const bool single = (op == FMMBEM_OP_SINGLE);
     const float b = (op == FMMBEM_OP_A) ? (float)(-c->f) : 1.f;
     apply_near(c, single, s.x, yg, b, st);
   }
-  if (timing) cudaEventRecord(c->ev[9], st);
+  if (timing) cudaEventRecord(c->ev[E_NEAR1], st);
+  c->timed_near = timing;
 }
 
 void apply_A(fmmbem_ctx* c, const float* x, float* y, cudaStream_t s) { apply_op(c, FMMBEM_OP_A, x, y, s, false); }
@@ -342,33 +369,25 @@ void partition(fmmbem_ctx* c, cudaStream_t st) {
 }
 
 void fill_timing(fmmbem_ctx* c, bool direct) {
-  float t[5] = {0, 0, 0, 0, 0};
-  cudaEventSynchronize(c->ev[4]);
-  for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], c->ev[i], c->ev[i + 1]);
   fmmbem_timing& T = c->last;
   const double g = T.gmres;
   std::memset(&T, 0, sizeof(T));
   T.gmres = g;
-  T.upward = t[0];
-  if (c->timed_comm) {
-    float tc = 0, ta = 0;
-    cudaEventElapsedTime(&tc, c->ev[5], c->ev[6]);  // multipole all-reduce
-    cudaEventElapsedTime(&ta, c->ev[7], c->ev[0]);  // x all-gather
-    T.comm = tc + ta;
-    T.upward -= tc;
-    T.total += ta;
+  if (!c->timed_near) return;
+  cudaEventSynchronize(c->ev[E_NEAR1]);
+  auto el = [&](int a, int b) {
+    float ms = 0.f;
+    return cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) == cudaSuccess ? (double)ms : 0.0;
+  };
+  if (!direct) {
+    T.upward = el(E_UP0, E_UP1);
+    T.m2l = el(E_M2L0, E_M2L1);
+    T.l2p = el(E_M2L1, E_DN1) + el(E_L2P0, E_L2P1);  // L2L + L2P
   }
-  float tm = 0;
-  cudaEventElapsedTime(&tm, c->ev[1], c->ev[8]);  // M2L alone; L2L is counted with L2P (downward)
-  T.m2l = tm;
-  T.p2p = t[2];
-  T.l2p = t[3] + (t[1] - tm);
-  T.total += t[0] + t[1] + t[2] + t[3];
-  float tn = 0;
-  if (cudaEventElapsedTime(&tn, c->ev[4], c->ev[9]) == cudaSuccess) {
-    T.near = tn;
-    T.total += tn;
-  }
+  T.p2p = el(E_P2P0, E_P2P1);
+  T.near = el(E_L2P1, E_NEAR1);
+  if (c->timed_comm) T.comm = el(E_AR0, E_AR1) + el(E_AG0, E_AG1);
+  T.total = el(E_AG0, E_NEAR1);  // wall time of the whole product (overlapped phases counted once)
   T.p2p_interactions = c->p2p_inter_kp;
   T.m2l_pairs = direct ? 0 : c->m2l_pairs_kp;
 }
@@ -455,9 +474,15 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   DevGuard dg(c->device);
   FMM_CUDA(cudaSetDevice(c->device));
   FMM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  FMM_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   c->P = opt.terms;
   if (const char* e = std::getenv("FMMBEM_M2L")) c->m2l_mode = (std::string(e) == "p4") ? 1 : 0;
+  // near field concurrent with the far field: default on with several ranks (hides the exchange)
+  c->overlap = opt.nranks > 1 ? 1 : 0;
+  if (const char* e = std::getenv("FMMBEM_OVERLAP")) c->overlap = std::atoi(e);
   c->NC = c->P * (c->P + 1) / 2;
   c->K = opt.quad_points;
   c->eps_in = eps_in;
@@ -566,8 +591,12 @@ void fmmbem_destroy(fmmbem_ctx* c) {
       comm_destroy(c);
     } catch (...) {
     }
+    if (c->side) cudaStreamSynchronize(c->side);
     for (auto& e : c->ev)
       if (e) cudaEventDestroy(e);
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
+    if (c->side) cudaStreamDestroy(c->side);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
   }

@@ -116,6 +116,10 @@ struct fmmbem_ctx {
   fmm::NearCSR near;                           // near_mode = 1 corrections
   int64_t n_own() const { return pan_hi - pan_lo; }
   fmmbem_timing last{};
-  cudaEvent_t ev[10] = {};
-  bool timed_comm = false;
+  // phase events (E_* in api.cu); recorded on the stream that runs the phase
+  cudaEvent_t ev[16] = {};
+  cudaEvent_t fork = nullptr, join = nullptr;  // untimed fork/join of the P2P side stream
+  cudaStream_t side = nullptr;                 // P2P runs here when overlap is on
+  int overlap = 0;                             // 1: P2P concurrent with the upward/M2L/exchange chain
+  bool timed_comm = false, timed_near = false;
 };
