@@ -191,40 +191,37 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     if (timing) cudaEventRecord(c->ev[e], q);
   };
   rec(E_START, st);
+  // with overlap the far-field chain (upward sweep, multipole exchange, M2L, L2L) runs on a
+  // high-priority internal stream and the near field on the caller's stream: the block scheduler
+  // gives the chain (and NCCL) SMs first and P2P fills the rest
   const bool ovl = c->overlap && !direct;
-  cudaStream_t ps = ovl ? c->side : st;
+  cudaStream_t fs = ovl ? c->side : st;
   if (ovl) {
     FMM_CUDA(cudaEventRecord(c->fork, st));
-    FMM_CUDA(cudaStreamWaitEvent(ps, c->fork, 0));
-    rec(E_P2P0, ps);
-    launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, ps);
-    rec(E_P2P1, ps);
-    FMM_CUDA(cudaEventRecord(c->join, ps));
+    FMM_CUDA(cudaStreamWaitEvent(fs, c->fork, 0));
   }
   if (!direct) {
-    rec(E_UP0, st);
-    launch_upward(c, s, st);
-    rec(E_UP1, st);
+    rec(E_UP0, fs);
+    launch_upward(c, s, fs);
+    rec(E_UP1, fs);
     if (distributed) {  // partial multipoles of the owned subtrees -> every cell's full multipole
-      rec(E_AR0, st);
+      rec(E_AR0, fs);
       const size_t off = (size_t)c->tree.lvl_off[2] * c->NC;
-      comm_allreduce_f32(c, reinterpret_cast<float*>(c->Mx.get() + off), 2 * (c->Mx.n - off), st);
-      rec(E_AR1, st);
+      comm_allreduce_f32(c, reinterpret_cast<float*>(c->Mx.get() + off), 2 * (c->Mx.n - off), fs);
+      rec(E_AR1, fs);
     }
     const int* tcnt = t.cnt ? t.cnt : t.set->cell_cnt.get();
-    rec(E_M2L0, st);
-    launch_m2l(c, s.set->cell_cnt.get(), tcnt, st);
-    rec(E_M2L1, st);
-    launch_downward(c, tcnt, st);
-    rec(E_DN1, st);
+    rec(E_M2L0, fs);
+    launch_m2l(c, s.set->cell_cnt.get(), tcnt, fs);
+    rec(E_M2L1, fs);
+    launch_downward(c, tcnt, fs);
+    rec(E_DN1, fs);
   }
-  if (!ovl) {
-    rec(E_P2P0, st);
-    launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
-    rec(E_P2P1, st);
-  } else {
-    FMM_CUDA(cudaStreamWaitEvent(st, c->join, 0));
-  }
+  if (ovl) FMM_CUDA(cudaEventRecord(c->join, fs));
+  rec(E_P2P0, st);
+  launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
+  rec(E_P2P1, st);
+  if (ovl) FMM_CUDA(cudaStreamWaitEvent(st, c->join, 0));
   rec(E_L2P0, st);
   if (!direct) {
     Outputs acc = o;
@@ -474,7 +471,11 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   DevGuard dg(c->device);
   FMM_CUDA(cudaSetDevice(c->device));
   FMM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  FMM_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;  // hi = greatest priority (numerically lowest)
+    FMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FMM_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+  }
   for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
   FMM_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
