@@ -204,10 +204,14 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     rec(E_UP0, fs);
     launch_upward(c, s, fs);
     rec(E_UP1, fs);
-    if (distributed) {  // partial multipoles of the owned subtrees -> every cell's full multipole
+    if (distributed) {  // the multipoles this rank's interaction lists need (LET)
       rec(E_AR0, fs);
-      const size_t off = (size_t)c->tree.lvl_off[2] * c->NC;
-      comm_allreduce_f32(c, reinterpret_cast<float*>(c->Mx.get() + off), 2 * (c->Mx.n - off), fs);
+      if (c->let.ready) {
+        exchange_let(c, fs);
+      } else {  // fallback: sum every rank's partial multipoles of levels >= 2
+        const size_t off = (size_t)c->tree.lvl_off[2] * c->NC;
+        comm_allreduce_f32(c, reinterpret_cast<float*>(c->Mx.get() + off), 2 * (c->Mx.n - off), fs);
+      }
       rec(E_AR1, fs);
     }
     const int* tcnt = t.cnt ? t.cnt : t.set->cell_cnt.get();
@@ -338,6 +342,7 @@ void partition(fmmbem_ctx* c, cudaStream_t st) {
   const int R = c->nranks;
   std::vector<int64_t> bounds(R + 1);
   split_costs(hc.data(), nl, R, bounds.data());
+  c->leaf_bounds = bounds;
   c->leaf_lo = (int)bounds[c->rank];
   c->leaf_hi = (int)bounds[c->rank + 1];
   c->pan_offs.assign(R + 1, 0);
@@ -557,6 +562,8 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   if (c->nranks > 1) {
     comm_init(c, opt.nccl_id);
     partition(c, s);
+    const char* e = std::getenv("FMMBEM_LET");
+    if (!(c->opt.direct != 0 || c->tree.L < 2) && !(e && std::atoi(e) == 0)) build_let(c, c->leaf_bounds, s);
   }
   if (c->opt.near_mode == 1) build_near(c, dV.get(), dT.get(), cen.get(), nrm.get(), area.get(), beta.get(), wq.get(), s);
   dV.release();

@@ -27,6 +27,8 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
@@ -50,6 +52,8 @@ NcclApi& api() {
   a.commDestroy = (decltype(a.commDestroy))sym("ncclCommDestroy");
   a.allReduce = (decltype(a.allReduce))sym("ncclAllReduce");
   a.broadcast = (decltype(a.broadcast))sym("ncclBroadcast");
+  a.send = (decltype(a.send))sym("ncclSend");
+  a.recv = (decltype(a.recv))sym("ncclRecv");
   a.groupStart = (decltype(a.groupStart))sym("ncclGroupStart");
   a.groupEnd = (decltype(a.groupEnd))sym("ncclGroupEnd");
   a.errStr = (decltype(a.errStr))sym("ncclGetErrorString");
@@ -103,6 +107,19 @@ void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const st
     check(api().broadcast(r == c->opt.rank ? (const void*)mine : (const void*)(full + offs[r]), full + offs[r], n,
                           ncclFloat32, r, (ncclComm_t)c->comm, s),
           "ncclBroadcast");
+  }
+  check(api().groupEnd(), "ncclGroupEnd");
+}
+
+// grouped point-to-point exchange: sbuf[p] (scnt[p] floats) -> rank p, rbuf[p] <- rank p
+void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std::vector<size_t>& scnt,
+                       const std::vector<float*>& rbuf, const std::vector<size_t>& rcnt, cudaStream_t s) {
+  const int R = c->opt.nranks;
+  check(api().groupStart(), "ncclGroupStart");
+  for (int p = 0; p < R; ++p) {
+    if (p == c->opt.rank) continue;
+    if (scnt[p]) check(api().send(sbuf[p], scnt[p], ncclFloat32, p, (ncclComm_t)c->comm, s), "ncclSend");
+    if (rcnt[p]) check(api().recv(rbuf[p], rcnt[p], ncclFloat32, p, (ncclComm_t)c->comm, s), "ncclRecv");
   }
   check(api().groupEnd(), "ncclGroupEnd");
 }

@@ -62,6 +62,17 @@ struct NearCSR {
   DevBuf<float> vkp, vsl, diag;
 };
 
+// local-essential-tree multipole exchange (let.cu)
+struct LetPlan {
+  bool ready = false;
+  std::vector<DevBuf<int>> send, recv;  // per peer: cells (global index), increasing
+  std::vector<int> nsend, nrecv;
+  DevBuf<int> shared;                   // cells straddling a rank boundary (partial on several ranks)
+  int nshared = 0;
+  DevBuf<float2> sbuf, rbuf, shbuf;
+  int64_t cells_sent = 0, cells_recv = 0;
+};
+
 struct Timing {
   cudaEvent_t ev[12];
   bool valid = false;
@@ -114,6 +125,8 @@ struct fmmbem_ctx {
   fmm::DevBuf<int> pan_own_cnt, quad_own_cnt;  // subtree counts of owned points
   fmm::DevBuf<float> xfull;                    // all-gathered source weights
   fmm::NearCSR near;                           // near_mode = 1 corrections
+  fmm::LetPlan let;                            // multipole LET exchange plan (nranks > 1)
+  std::vector<int64_t> leaf_bounds;            // [nranks + 1] leaf partition
   int64_t n_own() const { return pan_hi - pan_lo; }
   fmmbem_timing last{};
   // phase events (E_* in api.cu); recorded on the stream that runs the phase

@@ -59,6 +59,10 @@ void comm_allreduce_f64(fmmbem_ctx* c, double* buf, size_t n, cudaStream_t s);
 void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const std::vector<int64_t>& offs,
                          cudaStream_t s);
 void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds);
+void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std::vector<size_t>& scnt,
+                       const std::vector<float*>& rbuf, const std::vector<size_t>& rcnt, cudaStream_t s);
+void build_let(fmmbem_ctx* c, const std::vector<int64_t>& leaf_bounds, cudaStream_t s);
+void exchange_let(fmmbem_ctx* c, cudaStream_t s);
 // exact interaction count of launch_p2p(t, s) (list mode) -- setup-time helper
 int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct);
 
