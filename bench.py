@@ -311,7 +311,7 @@ def main():
                       "tree_levels": info["levels"], "n_leaves": info["n_leaves"],
                       "l2_flush": "inputs larger than L2 (x 409 MB, points 3.3 GB)",
                       "parallelism": "single GPU" if world == 1 else
-                      f"octree domain decomposition x{world} (NCCL all-gather x + all-reduce multipoles)"},
+                      f"octree domain decomposition x{world} (NCCL: all-gather x, LET multipole send/recv)"},
            "matvec_s": ms * 1e-3,
            "phases_ms": ph,
            "p2p_ginteractions_s": p2p_int / p2p_s / 1e9,
