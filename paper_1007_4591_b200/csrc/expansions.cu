@@ -16,140 +16,209 @@ namespace {
 
 __host__ __device__ constexpr int cx(int n, int m) { return n * (n + 1) / 2 + m; }
 
-// one order column m of the P2M sums of this lane's sources into the lane's slot
-template <int P, int m>
-__device__ __forceinline__ void p2m_column(float* slot, const float4* __restrict__ pos, const float* __restrict__ x,
-                                           int div, int b, int e, int lane, float inv_w) {
-  float ar[P - m], ai[P - m];
+constexpr int P2M_TILE = 128;  // sources staged in shared memory per pass
+
+// R_m^m(u) = (-(x + i y)/2)^m / m!
+template <int m>
+__device__ __forceinline__ void diag(float ux, float uy, float& rr, float& ri) {
+  rr = 1.f;
+  ri = 0.f;
 #pragma unroll
-  for (int k = 0; k < P - m; ++k) ar[k] = ai[k] = 0.f;
-  for (int j = b + lane; j < e; j += 32) {
-    const float4 p = __ldg(pos + j);
-    float w = p.w;
-    if (x) w *= __ldg(x + (div == 1 ? j : j / div));
-    const float ux = p.x * inv_w, uy = p.y * inv_w, uz = p.z * inv_w;
-    const float r2 = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-    float rr = 1.f, ri = 0.f;  // R_m^m = (-(x + i y)/2)^m / m!
-#pragma unroll
-    for (int k = 1; k <= m; ++k) {
-      const float s = -0.5f / (float)k;
-      const float t = (rr * ux - ri * uy) * s;
-      ri = (rr * uy + ri * ux) * s;
-      rr = t;
-    }
-    float pr = 0.f, pi = 0.f, cr = rr, ci = ri;
-    ar[0] = fmaf(w, cr, ar[0]);
-    ai[0] = fmaf(-w, ci, ai[0]);
-#pragma unroll
-    for (int n = m + 1; n < P; ++n) {
-      const float inv = 1.f / (float)((n - m) * (n + m));
-      const float a = (float)(2 * n - 1) * inv * uz, bb = r2 * inv;
-      const float nr = a * cr - bb * pr, ni = a * ci - bb * pi;
-      pr = cr;
-      pi = ci;
-      cr = nr;
-      ci = ni;
-      ar[n - m] = fmaf(w, cr, ar[n - m]);
-      ai[n - m] = fmaf(-w, ci, ai[n - m]);
-    }
+  for (int k = 1; k <= m; ++k) {
+    const float s = -0.5f / (float)k;
+    const float t = (rr * ux - ri * uy) * s;
+    ri = (rr * uy + ri * ux) * s;
+    rr = t;
   }
-#pragma unroll
-  for (int n = m; n < P; ++n) {
-    slot[(2 * cx(n, m)) * 33] = ar[n - m];
-    slot[(2 * cx(n, m) + 1) * 33] = ai[n - m];
-  }
-  if constexpr (m + 1 < P) p2m_column<P, m + 1>(slot, pos, x, div, b, e, lane, inv_w);
 }
 
+// accumulate column m of w conj(R_n^m(u)), n = m..P-1, into a[] (re, im packed)
+template <int P, int m>
+__device__ __forceinline__ void column_acc(float2 (&a)[P - m], float4 u, float r2) {
+  float cr, ci;
+  diag<m>(u.x, u.y, cr, ci);
+  float pr = 0.f, pi = 0.f;
+  const float2 nw = make_float2(u.w, -u.w);
+  a[0] = __ffma2_rn(nw, make_float2(cr, ci), a[0]);
+#pragma unroll
+  for (int n = m + 1; n < P; ++n) {
+    const float inv = 1.f / (float)((n - m) * (n + m));
+    const float aa = (float)(2 * n - 1) * inv * u.z, bb = r2 * inv;
+    const float nr = aa * cr - bb * pr, ni = aa * ci - bb * pi;
+    pr = cr;
+    pi = ci;
+    cr = nr;
+    ci = ni;
+    a[n - m] = __ffma2_rn(nw, make_float2(cr, ci), a[n - m]);
+  }
+}
+
+// columns m and P-1-m together (P+1 coefficients, two independent recurrences per source)
+template <int P, int m>
+__device__ __forceinline__ void p2m_columns(float2* slot, const float4* src, int ns, int lane) {
+  constexpr int m2 = P - 1 - m;
+  float2 a[P - m], b[P - m2];
+#pragma unroll
+  for (int k = 0; k < P - m; ++k) a[k] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < P - m2; ++k) b[k] = make_float2(0.f, 0.f);
+  for (int j = lane; j < ns; j += 32) {
+    const float4 u = src[j];
+    const float r2 = fmaf(u.x, u.x, fmaf(u.y, u.y, u.z * u.z));
+    column_acc<P, m>(a, u, r2);
+    if constexpr (m2 != m) column_acc<P, m2>(b, u, r2);
+  }
+#pragma unroll
+  for (int n = m; n < P; ++n) slot[cx(n, m) * 33] = __fadd2_rn(slot[cx(n, m) * 33], a[n - m]);
+  if constexpr (m2 != m) {
+#pragma unroll
+    for (int n = m2; n < P; ++n) slot[cx(n, m2) * 33] = __fadd2_rn(slot[cx(n, m2) * 33], b[n - m2]);
+  }
+  if constexpr (m + 1 < m2) p2m_columns<P, m + 1>(slot, src, ns, lane);
+}
+
+// P2M, one warp per leaf: the leaf's sources are scaled into the cell frame and staged in shared
+// memory once (u = (y - c)/w, weight), then every lane accumulates its sources' columns in
+// registers (two columns at a time for ILP), partial sums go to a per-lane float2 slot and are
+// reduced over the 32 lanes in a fixed order (no atomics).
 template <int P>
 __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
                                               const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               float2* __restrict__ M) {
   constexpr int NC = P * (P + 1) / 2;
-  __shared__ float sv[2 * NC * 33];
+  __shared__ float2 sv[NC * 33];
+  __shared__ float4 src[P2M_TILE];
   const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
-  p2m_column<P, 0>(sv + lane, pos, x, div, b, e, lane, inv_w);
+  for (int c = 0; c < NC; ++c) sv[c * 33 + lane] = make_float2(0.f, 0.f);
+  for (int t0 = b; t0 < e; t0 += P2M_TILE) {
+    const int ns = min(P2M_TILE, e - t0);
+    __syncwarp();
+    for (int k = lane; k < ns; k += 32) {
+      const int j = t0 + k;
+      const float4 p = __ldg(pos + j);
+      float w = p.w;
+      if (x) w *= __ldg(x + (div == 1 ? j : j / div));
+      src[k] = make_float4(p.x * inv_w, p.y * inv_w, p.z * inv_w, w);
+    }
+    __syncwarp();
+    p2m_columns<P, 0>(sv + lane, src, ns, lane);
+  }
   __syncwarp();
   for (int c = lane; c < NC; c += 32) {
-    float sx = 0.f, sy = 0.f;
-#pragma unroll 8
-    for (int l = 0; l < 32; ++l) {
-      sx += sv[(2 * c) * 33 + l];
-      sy += sv[(2 * c + 1) * 33 + l];
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+#pragma unroll
+    for (int l = 0; l < 32; l += 2) {
+      s0 = __fadd2_rn(s0, sv[c * 33 + l]);
+      s1 = __fadd2_rn(s1, sv[c * 33 + l + 1]);
     }
-    M[(size_t)(leaf_off + leaf) * NC + c] = make_float2(sx, sy);
+    M[(size_t)(leaf_off + leaf) * NC + c] = __fadd2_rn(s0, s1);
   }
 }
 
-template <int P>
+// L2P, one warp per leaf, lane = target.  Everything that does not depend on the target is done
+// once per leaf: the warp turns the leaf's local expansion into coefficient pairs for the
+// potential and the three gradient components (grad of sum L_n^m R_n^m lowers the degree:
+// d/dz -> L_{n+1}^m, d/dx -/+ i d/dy -> L_{n+1}^{m-1}, L_{n+1}^{m+1}), stored as
+//   gxy[c] = (X.re, Y.re, X.im, Y.im),  zph[c] = (Z.re, Phi.re, Z.im, Phi.im)
+// so that per target and coefficient (cr + i ci) = R_n^m(u) the update is
+//   (gx, gy) += (X.re, Y.re) cr + (X.im, Y.im) ci,  (gz, ph) += (Z.re, Phi.re) cr + (Z.im, Phi.im) ci
+// -- four packed FP32x2 FMAs; the recurrence for R_n^m is packed over (re, im) as well.
+template <int P, bool POT, bool DN>
 __global__ void __launch_bounds__(32) k_l2p_t(const float4* __restrict__ pos, const float4* __restrict__ nrm,
                                               const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               const float2* __restrict__ Lx, OutArg pot, OutArg dn) {
   constexpr int NC = P * (P + 1) / 2;
-  __shared__ float2 sl[NC + 1];
+  __shared__ float2 sl[NC];
+  __shared__ float4 gxy[NC], zph[NC];
   const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
   for (int c = lane; c < NC; c += 32) sl[c] = Lx[(size_t)(leaf_off + leaf) * NC + c];
-  if (lane == 0) sl[NC] = make_float2(0.f, 0.f);
   __syncwarp();
-  const bool want_pot = pot.y != nullptr, want_dn = dn.y != nullptr;
+  for (int c = lane; c < NC; c += 32) {
+    int n = 0;
+    while (cx(n + 1, 0) <= c) ++n;
+    const int m = c - cx(n, 0);
+    const float cm = (m == 0) ? 1.f : 2.f;
+    const float2 Ln = sl[c];
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f), z = make_float4(0.f, cm * Ln.x, 0.f, -cm * Ln.y);
+    if (n + 1 < P) {
+      const float2 Lz = sl[cx(n + 1, m)];
+      float2 Lm;
+      if (m == 0) {  // L_{n+1}^{-1} = -conj(L_{n+1}^1)
+        const float2 t = sl[cx(n + 1, 1)];
+        Lm = make_float2(-t.x, t.y);
+      } else {
+        Lm = sl[cx(n + 1, m - 1)];
+      }
+      const float2 Lp = sl[cx(n + 1, m + 1)];
+      // gx += 0.5 cm Re((dmr + i dmi)(cr + i ci)), gy += 0.5 cm (cr smi + ci smr)
+      g = make_float4(0.5f * cm * (Lm.x - Lp.x), 0.5f * cm * (Lm.y + Lp.y), -0.5f * cm * (Lm.y - Lp.y),
+                      0.5f * cm * (Lm.x + Lp.x));
+      z.x = cm * Lz.x;
+      z.z = -cm * Lz.y;
+    }
+    gxy[c] = g;
+    zph[c] = z;
+  }
+  __syncwarp();
   for (int i = b + lane; i < e; i += 32) {
     const float4 p = pos[i];
     const float ux = p.x * inv_w, uy = p.y * inv_w, uz = p.z * inv_w;
     const float r2 = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-    float ph = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
+    float2 gxy2 = make_float2(0.f, 0.f), gzph = make_float2(0.f, 0.f);
     float dr = 1.f, di = 0.f;
 #pragma unroll
     for (int m = 0; m < P; ++m) {
+      asm volatile("" ::: "memory");  // re-read the tables per column (no hoisting over the target loop)
       if (m > 0) {
         const float s = -0.5f / (float)m;
         const float t = (dr * ux - di * uy) * s;
         di = (dr * uy + di * ux) * s;
         dr = t;
       }
-      const float cm = (m == 0) ? 1.f : 2.f;
-      float pr = 0.f, pi = 0.f, cr = dr, ci = di;
+      float2 cur = make_float2(dr, di), prev = make_float2(0.f, 0.f);
 #pragma unroll
       for (int n = m; n < P; ++n) {
         if (n > m) {
           const float inv = 1.f / (float)((n - m) * (n + m));
           const float a = (float)(2 * n - 1) * inv * uz, bb = r2 * inv;
-          const float nr = a * cr - bb * pr, ni = a * ci - bb * pi;
-          pr = cr;
-          pi = ci;
-          cr = nr;
-          ci = ni;
+          const float2 nxt = __ffma2_rn(make_float2(a, a), cur, __fmul2_rn(make_float2(-bb, -bb), prev));
+          prev = cur;
+          cur = nxt;
         }
-        const float2 Ln = sl[cx(n, m)];
-        ph = fmaf(cm, Ln.x * cr - Ln.y * ci, ph);
-        if (n + 1 < P) {
-          const float2 Lz = sl[cx(n + 1, m)];
-          gz = fmaf(cm, Lz.x * cr - Lz.y * ci, gz);
-          float2 Lm;
-          if (m == 0) {  // L_{n+1}^{-1} = -conj(L_{n+1}^1)
-            const float2 t = sl[cx(n + 1, 1)];
-            Lm = make_float2(-t.x, t.y);
-          } else {
-            Lm = sl[cx(n + 1, m - 1)];
-          }
-          const float2 Lp = sl[cx(n + 1, m + 1)];
-          const float dmr = Lm.x - Lp.x, dmi = Lm.y - Lp.y, smr = Lm.x + Lp.x, smi = Lm.y + Lp.y;
-          gx = fmaf(0.5f * cm, cr * dmr - ci * dmi, gx);
-          gy = fmaf(0.5f * cm, cr * smi + ci * smr, gy);
+        const int c = cx(n, m);
+        if (DN && n + 1 < P) {
+          const float4 g = gxy[c];
+          gxy2 = __ffma2_rn(make_float2(g.x, g.y), make_float2(cur.x, cur.x), gxy2);
+          gxy2 = __ffma2_rn(make_float2(g.z, g.w), make_float2(cur.y, cur.y), gxy2);
+        }
+        if (POT || (DN && n + 1 < P)) {
+          const float4 z = zph[c];
+          gzph = __ffma2_rn(make_float2(z.x, z.y), make_float2(cur.x, cur.x), gzph);
+          gzph = __ffma2_rn(make_float2(z.z, z.w), make_float2(cur.y, cur.y), gzph);
         }
       }
     }
-    if (want_pot) pot.y[i] += pot.b * ph * inv_w;
-    if (want_dn) {
+    if (POT) pot.y[i] += pot.b * gzph.y * inv_w;
+    if (DN) {
       const float4 nn = nrm[i];
-      dn.y[i] += dn.b * (nn.x * gx + nn.y * gy + nn.z * gz) * inv_w * inv_w;
+      dn.y[i] += dn.b * (nn.x * gxy2.x + nn.y * gxy2.y + nn.z * gzph.x) * inv_w * inv_w;
     }
   }
+}
+
+template <int P>
+void l2p_dispatch(int grid, const float4* pos, const float4* nrm, const int* beg, float inv_w, int leaf_off, int leaf0,
+                  const float2* Lx, const OutArg& pot, const OutArg& dn, cudaStream_t st) {
+  const bool wp = pot.y != nullptr, wd = dn.y != nullptr;
+  if (wp && wd) k_l2p_t<P, true, true><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn);
+  else if (wp) k_l2p_t<P, true, false><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn);
+  else if (wd) k_l2p_t<P, false, true><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn);
 }
 
 }  // namespace
@@ -173,10 +242,10 @@ void launch_l2p_t(int P, int grid, const float4* pos, const float4* nrm, const i
                   int leaf0, const float2* Lx, const OutArg& pot, const OutArg& dn, cudaStream_t st) {
   if (grid <= 0) return;
   switch (P) {
-    case 8: k_l2p_t<8><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
-    case 10: k_l2p_t<10><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
-    case 12: k_l2p_t<12><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
-    case 14: k_l2p_t<14><<<grid, 32, 0, st>>>(pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn); break;
+    case 8: l2p_dispatch<8>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
+    case 10: l2p_dispatch<10>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
+    case 12: l2p_dispatch<12>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
+    case 14: l2p_dispatch<14>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
     default: throw Error(FMMBEM_E_INVALID, "L2P not specialised for this P");
   }
   FMM_CHECK_LAUNCH();

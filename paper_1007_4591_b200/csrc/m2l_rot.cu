@@ -87,6 +87,7 @@ __device__ __forceinline__ void pass_a(const Slot& sl, const float2* __restrict_
                                        const float (&zai)[P], const float (&zbr)[P], const float (&zbi)[P],
                                        float scale, float irho) {
   constexpr int c0 = n * (n + 1) / 2;
+  asm volatile("" ::: "memory");  // keep the degree blocks' loads in place (register pressure)
   float ar[n + 1], ai[n + 1], br[n + 1], bi[n + 1];
 #pragma unroll
   for (int m = 0; m <= n; ++m) {
@@ -107,6 +108,7 @@ __device__ __forceinline__ void pass_a(const Slot& sl, const float2* __restrict_
 // coaxial translation of order column k (input scaled by rho^-n, output missing rho^-(j+1))
 template <int P, int k>
 __device__ __forceinline__ void pass_b(const Slot& sl) {
+  asm volatile("" ::: "memory");
   float2 t[P - k];
 #pragma unroll
   for (int n = k; n < P; ++n) t[n - k] = sl.get(n * (n + 1) / 2 + k);
@@ -126,6 +128,7 @@ template <int P, int n>
 __device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], const float (&zai)[P],
                                        const float (&zbr)[P], const float (&zbi)[P], float scale, float irho) {
   constexpr int c0 = n * (n + 1) / 2;
+  asm volatile("" ::: "memory");
   float ar[n + 1], ai[n + 1], br[n + 1], bi[n + 1];
 #pragma unroll
   for (int m = 0; m <= n; ++m) {

@@ -2,8 +2,10 @@
 // contribution is obtained from directly computing the interactions between all the points
 // in the adjacent cells", "P2P ... the largest fractions").
 //
-// Work unit = one warp = one chunk of <= 64 targets of one leaf (T = 2 targets per lane in
-// registers; T = 4 with two source halves measured 2% slower).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
+// Work unit = one warp = one chunk of <= 64 targets of one leaf (T = 4 targets per lane in
+// registers as two packed FP32x2 pairs; measured at C5: T = 8 or 128-target chunks are slower --
+// registers -- and so is a scaled-coordinate form with one FP32x2 op fewer per interaction: the
+// loop is latency-, not issue-bound).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
 // and a tail chunk with few targets spreads its lanes over S source subsets (split-K, reduced in
 // shared memory) -- lanes stay busy whatever the occupancy.  The sources of the (<= 27)
 // neighbour leaves stream through a warp-private shared-memory tile, already shifted into the
@@ -276,14 +278,19 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   }
 }
 
-constexpr int P2P_T = 4;      // targets per lane: two packed FP32x2 pairs per shared-memory source load
-constexpr int P2P_CHUNK = 64; // targets per work item (16 lanes x 4 targets x 2 source halves)
+// targets per lane (pairs of packed FP32x2 targets per shared-memory source load) and targets per
+// work item; FMMBEM_P2P_T = 8 selects 4 pairs per lane (experiment knob)
+template <int T, bool SELF, bool CHECK>
+void dispatch_t(const P2PArgs& a, bool pot, bool dn, int grid, cudaStream_t st) {
+  if (pot && dn) k_p2p<T, true, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+  else if (pot) k_p2p<T, true, false, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+  else k_p2p<T, false, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+}
 
 template <bool SELF, bool CHECK>
-void dispatch(const P2PArgs& a, bool pot, bool dn, int grid, cudaStream_t st) {
-  if (pot && dn) k_p2p<P2P_T, true, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
-  else if (pot) k_p2p<P2P_T, true, false, SELF, CHECK><<<grid, 32, 0, st>>>(a);
-  else k_p2p<P2P_T, false, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+void dispatch(const P2PArgs& a, int t, bool pot, bool dn, int grid, cudaStream_t st) {
+  if (t == 8) dispatch_t<8, SELF, CHECK>(a, pot, dn, grid, st);
+  else dispatch_t<4, SELF, CHECK>(a, pot, dn, grid, st);
 }
 
 __global__ void k_count(int nl, const int* __restrict__ tbeg, const int* __restrict__ sbeg,
@@ -324,7 +331,7 @@ const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int lea
   for (auto& w : c->p2p_cache)
     if (w->tgt == &t && w->leaf_lo == leaf_lo && w->leaf_hi == leaf_hi) return *w;
   const int nl = leaf_hi - leaf_lo;
-  const int chunk = P2P_CHUNK;
+  const int chunk = c->p2p_chunk;
   cudaStream_t st = c->stream;
   auto w = std::make_unique<P2PItems>();
   w->tgt = &t;
@@ -380,12 +387,13 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   a.flag = c->flag.get();
   if (dn && !a.tnrm) throw Error(FMMBEM_E_INVALID, "normal derivative requested at targets without normals");
   const int grid = (int)items.n;
+  const int tl = c->p2p_t;
   if (self) {
-    if (check) dispatch<true, true>(a, pot, dn, grid, st);
-    else dispatch<true, false>(a, pot, dn, grid, st);
+    if (check) dispatch<true, true>(a, tl, pot, dn, grid, st);
+    else dispatch<true, false>(a, tl, pot, dn, grid, st);
   } else {
-    if (check) dispatch<false, true>(a, pot, dn, grid, st);
-    else dispatch<false, false>(a, pot, dn, grid, st);
+    if (check) dispatch<false, true>(a, tl, pot, dn, grid, st);
+    else dispatch<false, false>(a, tl, pot, dn, grid, st);
   }
   FMM_CHECK_LAUNCH();
 }
