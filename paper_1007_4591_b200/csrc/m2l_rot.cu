@@ -33,9 +33,63 @@ namespace {
 
 constexpr int RMAX = 16;  // degrees covered by the rotation tables
 __host__ __device__ constexpr int tri3(int n) { return n * (n + 1) * (2 * n + 1) / 6; }  // sum_{k<n} (k+1)^2
-constexpr int TSZ = tri3(RMAX);
-// [matrix][E/F][degree block]: 0 = D^-1, 1 = D, 2 = D^T, 3 = D^-T
-__constant__ float c_rot[4][2][TSZ];
+// [matrix][degree block][m'][m]: 0 = D^-1, 1 = D, 2 = D^T, 3 = D^-T.  Entry (m', m) holds E_m'm when
+// n + m + m' is even and F_m'm when odd (the other one is a structural zero).  The table is
+// evaluated at COMPILE time: with b = +-pi/2 every power of cos(b/2), sin(b/2) collapses to
+// 2^-n (+-1)^(m'-m), and W^n = diag(1/f) d^n diag(f) only needs f_m^2 = (n+m)!(n-m)!, so
+//   W^n_m'm(+-pi/2) = 2^-n (n+m)!(n-m)! (+-1)^(m'-m) sum_k (-1)^(m'-m+k) / ((n+m-k)! k! (m'-m+k)! (n-m'-k)!)
+// is rational -- after unrolling every matrix entry is an FFMA immediate (no constant-cache
+// loads, no uniform-register traffic).  init_rot_tables() re-derives the table on the host from
+// Wigner's formula in double precision and refuses to run if they disagree.
+__host__ __device__ constexpr int pad4(int v) { return (v + 3) & ~3; }
+__host__ __device__ constexpr int boff(int n) {  // sum_{k<n} pad4((k+1)^2)
+  int o = 0;
+  for (int k = 0; k < n; ++k) o += pad4((k + 1) * (k + 1));
+  return o;
+}
+constexpr int RMAXC = 12;  // highest instantiated rotation order
+constexpr int TSZ = boff(RMAXC);
+struct RotTab {
+  float v[4][TSZ];
+};
+__host__ __device__ constexpr double cfact(int n) {
+  double f = 1.0;
+  for (int i = 2; i <= n; ++i) f *= (double)i;
+  return f;
+}
+__host__ __device__ constexpr double w_half_pi(int n, int mp, int m, int sgn) {  // W^n_{mp,m}(sgn pi/2)
+  double t = 0.0;
+  const int k0 = (m - mp) > 0 ? (m - mp) : 0, k1 = (n + m) < (n - mp) ? (n + m) : (n - mp);
+  for (int k = k0; k <= k1; ++k)
+    t += (((mp - m + k) & 1) ? -1.0 : 1.0) / (cfact(n + m - k) * cfact(k) * cfact(mp - m + k) * cfact(n - mp - k));
+  double sc = cfact(n + m) * cfact(n - m);
+  for (int i = 0; i < n; ++i) sc *= 0.5;
+  if (sgn < 0 && ((mp - m) & 1)) sc = -sc;
+  return t * sc;
+}
+__host__ __device__ constexpr double x_entry(int X, int n, int a, int b) {
+  return X == 0 ? w_half_pi(n, a, b, -1) : X == 1 ? w_half_pi(n, a, b, 1) : X == 2 ? w_half_pi(n, b, a, 1)
+                                                                               : w_half_pi(n, b, a, -1);
+}
+__host__ __device__ constexpr RotTab make_rot() {
+  RotTab t{};
+  for (int X = 0; X < 4; ++X)
+    for (int n = 0; n < RMAXC; ++n)
+      for (int mp = 0; mp <= n; ++mp)
+        for (int m = 0; m <= n; ++m) {
+          double v = 0.0;
+          if (m == 0) {
+            if (((n + mp) & 1) == 0) v = x_entry(X, n, mp, 0);  // E_m'0 = X_m'0, F_m'0 = 0
+          } else {
+            const double sg = (m & 1) ? -1.0 : 1.0;
+            v = ((n + m + mp) & 1) == 0 ? x_entry(X, n, mp, m) + sg * x_entry(X, n, mp, -m)
+                                        : x_entry(X, n, mp, m) - sg * x_entry(X, n, mp, -m);
+          }
+          t.v[X][boff(n) + mp * (n + 1) + m] = (float)v;
+        }
+  return t;
+}
+__device__ constexpr RotTab ROT = make_rot();
 
 __host__ __device__ constexpr float factf(int n) {
   float f = 1.f;
@@ -66,8 +120,8 @@ __device__ __forceinline__ void mat_block(const float (&ar)[n + 1], const float 
     for (int m = 0; m <= n; ++m) {
       // Wigner parity d_{m',-m}(pi/2) = (-1)^{n+m'} d_{m'm}(pi/2): E vanishes for odd n+m+m',
       // F for even n+m+m' -- half of the products are structural zeros and are skipped here
-      if (((n + m + mp) & 1) == 0) re = fmaf(c_rot[X][0][tri3(n) + mp * (n + 1) + m], ar[m], re);
-      else if (m > 0) im = fmaf(c_rot[X][1][tri3(n) + mp * (n + 1) + m], ai[m], im);
+      if (((n + m + mp) & 1) == 0) re = fmaf(ROT.v[X][boff(n) + mp * (n + 1) + m], ar[m], re);
+      else if (m > 0) im = fmaf(ROT.v[X][boff(n) + mp * (n + 1) + m], ai[m], im);
     }
     br[mp] = re;
     bi[mp] = im;
@@ -471,21 +525,15 @@ bool rot_supported(int P) { return P == 8 || P == 10 || P == 12; }
 void init_rot_tables() {
   static bool done = false;
   if (done) return;
-  std::vector<float> h(4 * 2 * TSZ, 0.f);
-  for (int n = 0; n < RMAX; ++n) {
+  static constexpr RotTab host = make_rot();  // the same compile-time table the kernels fold in
+  for (int n = 0; n < RMAXC; ++n) {
     std::vector<double> f(2 * n + 1);
-    for (int m = -n; m <= n; ++m) {
-      double a = 1, b = 1;
-      for (int i = 2; i <= n + m; ++i) a *= i;
-      for (int i = 2; i <= n - m; ++i) b *= i;
-      f[m + n] = std::sqrt(a * b);
-    }
-    // W(+pi/2) = D, W(-pi/2) = D^-1 in the R_n^m basis
+    for (int m = -n; m <= n; ++m) f[m + n] = std::sqrt(cfact(n + m) * cfact(n - m));
+    // W(+pi/2) = D, W(-pi/2) = D^-1 in the R_n^m basis, from Wigner's formula with cos/sin
     auto W = [&](int mp, int m, double beta) { return wigner_d(n, mp, m, beta) * f[m + n] / f[mp + n]; };
-    for (int X = 0; X < 4; ++X) {
+    for (int X = 0; X < 4; ++X)
       for (int mp = 0; mp <= n; ++mp)
         for (int m = 0; m <= n; ++m) {
-          // X_{mp,m} for X in {D^-1, D, D^T, D^-T}
           auto Xv = [&](int a, int b) {
             switch (X) {
               case 0: return W(a, b, -M_PI / 2);
@@ -494,21 +542,15 @@ void init_rot_tables() {
               default: return W(b, a, -M_PI / 2);
             }
           };
-          double e, g;
-          if (m == 0) {
-            e = Xv(mp, 0);
-            g = 0;
-          } else {
-            double sg = (m & 1) ? -1.0 : 1.0;
-            e = Xv(mp, m) + sg * Xv(mp, -m);
-            g = Xv(mp, m) - sg * Xv(mp, -m);
-          }
-          h[(X * 2 + 0) * TSZ + tri3(n) + mp * (n + 1) + m] = (float)e;
-          h[(X * 2 + 1) * TSZ + tri3(n) + mp * (n + 1) + m] = (float)g;
+          double v = 0.0;
+          const double sg = (m & 1) ? -1.0 : 1.0;
+          if (((n + m + mp) & 1) == 0) v = (m == 0) ? Xv(mp, 0) : Xv(mp, m) + sg * Xv(mp, -m);
+          else if (m > 0) v = Xv(mp, m) - sg * Xv(mp, -m);
+          const double got = host.v[X][boff(n) + mp * (n + 1) + m];
+          if (std::fabs(got - v) > 1e-6 * std::max(1.0, std::fabs(v)))
+            throw Error(FMMBEM_E_CUDA, "rotation table self-check failed");
         }
-    }
   }
-  FMM_CUDA(cudaMemcpyToSymbol(c_rot, h.data(), h.size() * sizeof(float)));
   done = true;
 }
 
