@@ -202,6 +202,107 @@ __device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], co
   if constexpr (n + 1 < P) pass_c<P, n + 1>(sl, zar, zai, zbr, zbi, scale * irho, irho);
 }
 
+// the translated local expansion of source cell s at target (tx, ty, tz) into the thread's slot
+template <int P>
+__device__ __forceinline__ void translate_pair(const Slot& sl, int tx, int ty, int tz, int s,
+                                               const uint64_t* __restrict__ key, const float2* __restrict__ M) {
+  constexpr int NC = P * (P + 1) / 2;
+  int sx, sy, sz;
+  demorton(key[s], sx, sy, sz);
+  const float dx = (float)(tx - sx), dy = (float)(ty - sy), dz = (float)(tz - sz);
+  const float rxy2 = dx * dx + dy * dy;
+  const float rxy = sqrtf(rxy2);
+  const float irho = rsqrtf(rxy2 + dz * dz);
+  float cp = 1.f, sp = 0.f;
+  if (rxy > 0.f) {
+    cp = dx / rxy;
+    sp = dy / rxy;
+  }
+  // powers of za = e^{i(p + pi/2)} = i e^{ip} and zb = e^{it}
+  float zar[P], zai[P], zbr[P], zbi[P];
+  zar[0] = 1.f;
+  zai[0] = 0.f;
+  zbr[0] = 1.f;
+  zbi[0] = 0.f;
+  const float ar1 = -sp, ai1 = cp, br1 = dz * irho, bi1 = rxy * irho;
+#pragma unroll
+  for (int m = 1; m < P; ++m) {
+    zar[m] = zar[m - 1] * ar1 - zai[m - 1] * ai1;
+    zai[m] = zar[m - 1] * ai1 + zai[m - 1] * ar1;
+    zbr[m] = zbr[m - 1] * br1 - zbi[m - 1] * bi1;
+    zbi[m] = zbr[m - 1] * bi1 + zbi[m - 1] * br1;
+  }
+  pass_a<P, 0>(sl, M + (size_t)s * NC, zar, zai, zbr, zbi, 1.f, irho);
+  pass_b<P, 0>(sl);
+  pass_c<P, 0>(sl, zar, zai, zbr, zbi, irho, irho);
+}
+
+// Lockstep variant: the W warps of a CTA (one target row each) start every 32-pair round together
+// (__syncthreads per round), so the SM's warps walk the long unrolled body in step and share the
+// instruction-cache lines (the body is ~3x the L1.5 I$); dynamic shared memory, W slots.
+template <int P, int W>
+__global__ void __launch_bounds__(32 * W) k_m2l_rot_sync(int rows, const int* __restrict__ tcells,
+                                                         const int* __restrict__ off, const int* __restrict__ idx,
+                                                         const uint64_t* __restrict__ key,
+                                                         const float2* __restrict__ M, float2* __restrict__ Lx) {
+  constexpr int NC = P * (P + 1) / 2;
+  constexpr int NR = (NC + 31) / 32;
+  extern __shared__ float2 svdyn[];
+  __shared__ int rounds_w[W];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * W + w;
+  const bool has = row < rows;
+  float2* sv = svdyn + (size_t)w * NC * 33;
+  const int cell = has ? tcells[row] : 0;
+  const int lo = has ? off[row] : 0, hi = has ? off[row + 1] : 0;
+  if (lane == 0) rounds_w[w] = (hi - lo + 31) / 32;
+  __syncthreads();
+  int rounds = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) rounds = max(rounds, rounds_w[k]);
+  const Slot sl{sv + lane};
+  int tx = 0, ty = 0, tz = 0;
+  if (has) demorton(key[cell], tx, ty, tz);
+  float2 acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = make_float2(0.f, 0.f);
+  for (int rd = 0; rd < rounds; ++rd) {
+    const int e0 = lo + 32 * rd;
+    if (e0 < hi) {
+      const int e = e0 + lane;
+      if (e < hi) {
+        translate_pair<P>(sl, tx, ty, tz, idx[e], key, M);
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sl.set(c, 0.f, 0.f);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int c = lane + 32 * r;
+        if (c < NC) {
+          float2 sum = make_float2(0.f, 0.f);
+#pragma unroll 8
+          for (int l = 0; l < 32; ++l) sum = __fadd2_rn(sum, sv[c * 33 + l]);
+          acc[r] = __fadd2_rn(acc[r], sum);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!has) return;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int c = lane + 32 * r;
+    if (c < NC) {
+      float2 o = Lx[(size_t)cell * NC + c];
+      o.x += acc[r].x;
+      o.y += acc[r].y;
+      Lx[(size_t)cell * NC + c] = o;
+    }
+  }
+}
+
 // one warp per target cell; W warps per CTA start in lockstep on the same (long, unrolled) code
 template <int P, int W>
 __global__ void __launch_bounds__(32 * W) k_m2l_rot(int rows, const int* __restrict__ tcells,
@@ -226,35 +327,7 @@ __global__ void __launch_bounds__(32 * W) k_m2l_rot(int rows, const int* __restr
   for (int e0 = lo; e0 < hi; e0 += 32) {
     const int e = e0 + lane;
     if (e < hi) {
-      const int s = idx[e];
-      int sx, sy, sz;
-      demorton(key[s], sx, sy, sz);
-      const float dx = (float)(tx - sx), dy = (float)(ty - sy), dz = (float)(tz - sz);
-      const float rxy2 = dx * dx + dy * dy;
-      const float rxy = sqrtf(rxy2);
-      const float irho = rsqrtf(rxy2 + dz * dz);
-      float cp = 1.f, sp = 0.f;
-      if (rxy > 0.f) {
-        cp = dx / rxy;
-        sp = dy / rxy;
-      }
-      // powers of za = e^{i(p + pi/2)} = i e^{ip} and zb = e^{it}
-      float zar[P], zai[P], zbr[P], zbi[P];
-      zar[0] = 1.f;
-      zai[0] = 0.f;
-      zbr[0] = 1.f;
-      zbi[0] = 0.f;
-      const float ar1 = -sp, ai1 = cp, br1 = dz * irho, bi1 = rxy * irho;
-#pragma unroll
-      for (int m = 1; m < P; ++m) {
-        zar[m] = zar[m - 1] * ar1 - zai[m - 1] * ai1;
-        zai[m] = zar[m - 1] * ai1 + zai[m - 1] * ar1;
-        zbr[m] = zbr[m - 1] * br1 - zbi[m - 1] * bi1;
-        zbi[m] = zbr[m - 1] * bi1 + zbi[m - 1] * br1;
-      }
-      pass_a<P, 0>(sl, M + (size_t)s * NC, zar, zai, zbr, zbi, 1.f, irho);
-      pass_b<P, 0>(sl);
-      pass_c<P, 0>(sl, zar, zai, zbr, zbi, irho, irho);
+      translate_pair<P>(sl, tx, ty, tz, idx[e], key, M);
     } else {
 #pragma unroll
       for (int c = 0; c < NC; ++c) sl.set(c, 0.f, 0.f);
@@ -311,11 +384,11 @@ __device__ __forceinline__ void rot_block(float (&ar)[n + 1], float (&ai)[n + 1]
   mat_block<n, XB>(br, bi, ar, ai);
 }
 
-// pass over degrees: (global src | slot) -> rot_block -> (slot | global dst (=, +=))
-template <int P, int n, int XA, int XB, int MODE>  // MODE 0: src -> slot, 1: slot -> dst (=), 2: slot -> dst (+=)
-__device__ __forceinline__ void rot_pass(const Slot& sl, const float2* __restrict__ src, float2* __restrict__ dst,
-                                         const float* zar, const float* zai, const float* zbr, const float* zbi,
-                                         float cs) {
+// pass over degrees, forward (MODE 0: global src -> slot, 3: slot -> slot) or back rotation
+// (4: slot -> slot); in-place slot passes are safe because degree block n only reads block n
+template <int P, int n, int XA, int XB, int MODE>
+__device__ __forceinline__ void rot_pass(const Slot& sl, const float2* __restrict__ src, const float* zar,
+                                         const float* zai, const float* zbr, const float* zbi) {
   constexpr int c0 = n * (n + 1) / 2;
   float ar[n + 1], ai[n + 1];
 #pragma unroll
@@ -330,7 +403,7 @@ __device__ __forceinline__ void rot_pass(const Slot& sl, const float2* __restric
       ai[m] = v.y;
     }
   }
-  if (MODE == 0) {
+  if (MODE != 4) {
     rot_block<n, XA, XB>(ar, ai, zar, zai, zbr, zbi, 1.f, 1.f);
 #pragma unroll
     for (int m = 0; m <= n; ++m) sl.set(c0 + m, ar[m], ai[m]);
@@ -344,16 +417,35 @@ __device__ __forceinline__ void rot_pass(const Slot& sl, const float2* __restric
 #pragma unroll
     for (int m = 0; m <= n; ++m) {
       if (m > 0) cmul_ip(ar[m], ai[m], zar[m], -zai[m]);
-      if (MODE == 1) {
-        dst[c0 + m] = make_float2(ar[m], ai[m]);
-      } else {
-        float2 o = dst[c0 + m];
-        dst[c0 + m] = make_float2(o.x + ar[m], o.y + ai[m]);
-      }
+      sl.set(c0 + m, ar[m], ai[m]);
     }
   }
-  (void)cs;
-  if constexpr (n + 1 < P) rot_pass<P, n + 1, XA, XB, MODE>(sl, src, dst, zar, zai, zbr, zbi, cs);
+  if constexpr (n + 1 < P) rot_pass<P, n + 1, XA, XB, MODE>(sl, src, zar, zai, zbr, zbi);
+}
+
+// warp-cooperative coalesced copies between a contiguous block of `cnt` cells' expansions in
+// global memory and the warp's per-lane slots (lane i <-> cell i)
+template <int NC>
+__device__ __forceinline__ void slots_load(float2* sv, const float2* __restrict__ g, int cnt, int lane) {
+  for (int k = lane; k < cnt * NC; k += 32) {
+    const int i = k / NC, c = k - i * NC;
+    sv[c * 33 + i] = g[k];
+  }
+}
+template <int NC, bool ADD>
+__device__ __forceinline__ void slots_store(const float2* sv, float2* __restrict__ g, int cnt, const int* __restrict__ on,
+                                            int lane) {
+  for (int k = lane; k < cnt * NC; k += 32) {
+    const int i = k / NC, c = k - i * NC;
+    if (on && !on[i]) continue;
+    const float2 v = sv[c * 33 + i];
+    if (ADD) {
+      const float2 o = g[k];
+      g[k] = make_float2(o.x + v.x, o.y + v.y);
+    } else {
+      g[k] = v;
+    }
+  }
 }
 
 // coaxial M2M along +z by RHO8: M_n^k <- sum_{j=k}^{n} 2^-j M_j^k rho^(n-j)/(n-j)!
@@ -411,23 +503,34 @@ __device__ __forceinline__ void octant_phases(uint64_t key, float* zar, float* z
   }
 }
 
-// thread per child cell at one level: T[child] = (translated child multipole); summed per parent below
+// thread per child cell at one level: T[child] = (translated child multipole); summed per parent below.
+// The warp's 32 children are contiguous: their multipoles come in and the results go out through
+// the slots with coalesced accesses.
 template <int P>
 __global__ void __launch_bounds__(32) k_m2m_rot(int c0, int n, const uint64_t* __restrict__ key,
                                                 const int* __restrict__ scnt, const float2* __restrict__ M,
                                                 float2* __restrict__ T) {
   constexpr int NC = P * (P + 1) / 2;
   __shared__ float2 sv[NC * 33];
-  const int i = blockIdx.x * 32 + threadIdx.x;
-  if (i >= n) return;
+  __shared__ int on[32];
+  const int lane = threadIdx.x;
+  const int b0 = blockIdx.x * 32, cnt = min(32, n - b0);
+  const int i = b0 + lane;
   const int cell = c0 + i;
-  if (scnt[cell] == 0) return;
-  const Slot sl{sv + threadIdx.x};
-  float zar[P], zai[P], zbr[P], zbi[P];
-  octant_phases<P>(key[cell], zar, zai, zbr, zbi);
-  rot_pass<P, 0, 0, 1, 0>(sl, M + (size_t)cell * NC, nullptr, zar, zai, zbr, zbi, 1.f);
-  coax_m2m<P, 0>(sl);
-  rot_pass<P, 0, 0, 1, 1>(sl, nullptr, T + (size_t)cell * NC, zar, zai, zbr, zbi, 1.f);
+  const bool act = i < n && scnt[cell] > 0;
+  on[lane] = act;
+  slots_load<NC>(sv, M + (size_t)(c0 + b0) * NC, cnt, lane);
+  __syncwarp();
+  const Slot sl{sv + lane};
+  if (act) {
+    float zar[P], zai[P], zbr[P], zbi[P];
+    octant_phases<P>(key[cell], zar, zai, zbr, zbi);
+    rot_pass<P, 0, 0, 1, 3>(sl, nullptr, zar, zai, zbr, zbi);
+    coax_m2m<P, 0>(sl);
+    rot_pass<P, 0, 0, 1, 4>(sl, nullptr, zar, zai, zbr, zbi);
+  }
+  __syncwarp();
+  slots_store<NC, false>(sv, T + (size_t)(c0 + b0) * NC, cnt, on, lane);
 }
 
 // parent multipole = sum of its children's translated multipoles (fixed order)
@@ -448,23 +551,31 @@ __global__ void k_m2m_sum(int c0, int n, int NC, const int* __restrict__ cb, con
   M[(size_t)cell * NC + c] = s;
 }
 
-// thread per child cell: L[child] += translated parent local expansion
+// thread per child cell: L[child] += translated parent local expansion (coalesced accumulate of the
+// warp's 32 contiguous children through the slots)
 template <int P>
 __global__ void __launch_bounds__(32) k_l2l_rot(int c0, int n, const uint64_t* __restrict__ key,
                                                 const int* __restrict__ parent, const int* __restrict__ tcnt,
                                                 float2* __restrict__ Lx) {
   constexpr int NC = P * (P + 1) / 2;
   __shared__ float2 sv[NC * 33];
-  const int i = blockIdx.x * 32 + threadIdx.x;
-  if (i >= n) return;
+  __shared__ int on[32];
+  const int lane = threadIdx.x;
+  const int b0 = blockIdx.x * 32, cnt = min(32, n - b0);
+  const int i = b0 + lane;
   const int cell = c0 + i;
-  if (tcnt[cell] == 0) return;
-  const Slot sl{sv + threadIdx.x};
-  float zar[P], zai[P], zbr[P], zbi[P];
-  octant_phases<P>(key[cell], zar, zai, zbr, zbi);
-  rot_pass<P, 0, 2, 3, 0>(sl, Lx + (size_t)parent[cell] * NC, nullptr, zar, zai, zbr, zbi, 1.f);
-  coax_l2l<P, 0>(sl);
-  rot_pass<P, 0, 2, 3, 2>(sl, nullptr, Lx + (size_t)cell * NC, zar, zai, zbr, zbi, 1.f);
+  const bool act = i < n && tcnt[cell] > 0;
+  on[lane] = act;
+  const Slot sl{sv + lane};
+  if (act) {
+    float zar[P], zai[P], zbr[P], zbi[P];
+    octant_phases<P>(key[cell], zar, zai, zbr, zbi);
+    rot_pass<P, 0, 2, 3, 0>(sl, Lx + (size_t)parent[cell] * NC, zar, zai, zbr, zbi);
+    coax_l2l<P, 0>(sl);
+    rot_pass<P, 0, 2, 3, 4>(sl, nullptr, zar, zai, zbr, zbi);
+  }
+  __syncwarp();
+  slots_store<NC, true>(sv, Lx + (size_t)(c0 + b0) * NC, cnt, on, lane);
 }
 
 // Wigner small d^n_{m'm}(b) (explicit sum)
@@ -624,6 +735,18 @@ void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st) {
   FMM_CHECK_LAUNCH();
 }
 
+template <int P, int W>
+void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k_m2l_rot_sync<P, W><<<ceil_div(w.rows, W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
+                                                                   w.idx.get(), T.key.get(), c->Mx.get(),
+                                                                   c->Lx.get());
+}
+
 void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
   if (w.rows == 0) return;
   const Tree& T = c->tree;
@@ -633,7 +756,14 @@ void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
   }();
 #define FMM_ROT_CASE(PP)                                                                                     \
   case PP:                                                                                                   \
-    if (warps == 2)                                                                                          \
+    if (warps >= 3) {                                                                                        \
+      const size_t smem = (size_t)warps * (PP * (PP + 1) / 2) * 33 * sizeof(float2);                        \
+      switch (warps) {                                                                                       \
+        case 4: m2l_sync_launch<PP, 4>(w, T, c, smem, st); break;                                            \
+        case 8: m2l_sync_launch<PP, 8>(w, T, c, smem, st); break;                                            \
+        default: m2l_sync_launch<PP, 10>(w, T, c, smem, st); break;                                          \
+      }                                                                                                      \
+    } else if (warps == 2)                                                                                   \
       k_m2l_rot<PP, 2><<<ceil_div(w.rows, 2), 64, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(),          \
                                                             w.idx.get(), T.key.get(), c->Mx.get(), c->Lx.get()); \
     else                                                                                                     \
