@@ -34,8 +34,6 @@ namespace fmm {
 
 namespace {
 
-constexpr int RMAX = 16;  // degrees covered by the rotation tables
-__host__ __device__ constexpr int tri3(int n) { return n * (n + 1) * (2 * n + 1) / 6; }  // sum_{k<n} (k+1)^2
 // [matrix][degree block][m'][m]: 0 = D^-1, 1 = D, 2 = D^T, 3 = D^-T.  Entry (m', m) holds E_m'm when
 // n + m + m' is even and F_m'm when odd (the other one is a structural zero).  The table is
 // evaluated at COMPILE time: with b = +-pi/2 every power of cos(b/2), sin(b/2) collapses to
