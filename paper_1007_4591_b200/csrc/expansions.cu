@@ -53,9 +53,11 @@ __device__ __forceinline__ void column_acc(float2 (&a)[P - m], float4 u, float r
   }
 }
 
-// columns m and P-1-m together (P+1 coefficients, two independent recurrences per source)
+// columns m and P-1-m together (P+1 coefficients, two independent recurrences per source); the
+// lanes' partial sums are transposed through red[P+1][33] and lane c (< P+1) adds the 32 partials of
+// entry c to its register accumulator acc[m] (fixed order, no atomics)
 template <int P, int m>
-__device__ __forceinline__ void p2m_columns(float2* slot, const float4* src, int ns, int lane) {
+__device__ __forceinline__ void p2m_columns(float2 (&acc)[P / 2], float2* red, const float4* src, int ns, int lane) {
   constexpr int m2 = P - 1 - m;
   float2 a[P - m], b[P - m2];
 #pragma unroll
@@ -66,33 +68,45 @@ __device__ __forceinline__ void p2m_columns(float2* slot, const float4* src, int
     const float4 u = src[j];
     const float r2 = fmaf(u.x, u.x, fmaf(u.y, u.y, u.z * u.z));
     column_acc<P, m>(a, u, r2);
-    if constexpr (m2 != m) column_acc<P, m2>(b, u, r2);
+    column_acc<P, m2>(b, u, r2);
   }
 #pragma unroll
-  for (int n = m; n < P; ++n) slot[cx(n, m) * 33] = __fadd2_rn(slot[cx(n, m) * 33], a[n - m]);
-  if constexpr (m2 != m) {
+  for (int k = 0; k < P - m; ++k) red[k * 33 + lane] = a[k];
 #pragma unroll
-    for (int n = m2; n < P; ++n) slot[cx(n, m2) * 33] = __fadd2_rn(slot[cx(n, m2) * 33], b[n - m2]);
+  for (int k = 0; k < P - m2; ++k) red[(P - m + k) * 33 + lane] = b[k];
+  __syncwarp();
+  if (lane < P + 1) {
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+#pragma unroll
+    for (int l = 0; l < 32; l += 2) {
+      s0 = __fadd2_rn(s0, red[lane * 33 + l]);
+      s1 = __fadd2_rn(s1, red[lane * 33 + l + 1]);
+    }
+    acc[m] = __fadd2_rn(acc[m], __fadd2_rn(s0, s1));
   }
-  if constexpr (m + 1 < m2) p2m_columns<P, m + 1>(slot, src, ns, lane);
+  __syncwarp();
+  if constexpr (m + 1 < m2) p2m_columns<P, m + 1>(acc, red, src, ns, lane);
 }
 
 // P2M, one warp per leaf: the leaf's sources are scaled into the cell frame and staged in shared
 // memory once (u = (y - c)/w, weight), then every lane accumulates its sources' columns in
-// registers (two columns at a time for ILP), partial sums go to a per-lane float2 slot and are
-// reduced over the 32 lanes in a fixed order (no atomics).
+// registers (two columns at a time for ILP) and the column pair is reduced over the lanes at once,
+// so shared memory stays small (occupancy) whatever P.
 template <int P>
 __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
                                               const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               float2* __restrict__ M) {
+  static_assert(P % 2 == 0, "column pairs");
   constexpr int NC = P * (P + 1) / 2;
-  __shared__ float2 sv[NC * 33];
+  __shared__ float2 red[(P + 1) * 33];
   __shared__ float4 src[P2M_TILE];
   const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
-  for (int c = 0; c < NC; ++c) sv[c * 33 + lane] = make_float2(0.f, 0.f);
+  float2 acc[P / 2];
+#pragma unroll
+  for (int k = 0; k < P / 2; ++k) acc[k] = make_float2(0.f, 0.f);
   for (int t0 = b; t0 < e; t0 += P2M_TILE) {
     const int ns = min(P2M_TILE, e - t0);
     __syncwarp();
@@ -104,17 +118,18 @@ __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, co
       src[k] = make_float4(p.x * inv_w, p.y * inv_w, p.z * inv_w, w);
     }
     __syncwarp();
-    p2m_columns<P, 0>(sv + lane, src, ns, lane);
+    p2m_columns<P, 0>(acc, red, src, ns, lane);
   }
-  __syncwarp();
-  for (int c = lane; c < NC; c += 32) {
-    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+  if (lane < P + 1) {
+    float2* Mo = M + (size_t)(leaf_off + leaf) * NC;
 #pragma unroll
-    for (int l = 0; l < 32; l += 2) {
-      s0 = __fadd2_rn(s0, sv[c * 33 + l]);
-      s1 = __fadd2_rn(s1, sv[c * 33 + l + 1]);
+    for (int m = 0; m < P / 2; ++m) {
+      const int m2 = P - 1 - m;
+      // entry lane: (n = m + lane, m) for lane < P - m, else (n = m2 + lane - (P - m), m2)
+      const int n = lane < P - m ? m + lane : m2 + lane - (P - m);
+      const int mm = lane < P - m ? m : m2;
+      Mo[cx(n, mm)] = acc[m];
     }
-    M[(size_t)(leaf_off + leaf) * NC + c] = __fadd2_rn(s0, s1);
   }
 }
 
