@@ -152,8 +152,13 @@ SrcArg kp_src(fmmbem_ctx* c, const float* x_local, cudaStream_t st, bool* distri
   *distributed = false;
   if (multi(c)) {
     c->xfull.alloc(c->np);
-    comm_allgatherv_f32(c, x_local, c->xfull.get(), c->pan_offs, st);
     s.x = c->xfull.get();
+    s.x_far = x_local - c->pan_lo;  // P2M reads owned panels only: a global-index view of the slice
+    if (c->overlap && c->comm2) {
+      s.ag_src = x_local;  // all-gathered by fmm_eval on the caller's stream, behind the fork
+    } else {
+      comm_allgatherv_f32(c, x_local, c->xfull.get(), c->pan_offs, st);
+    }
     s.leaf_lo = c->leaf_lo;
     s.leaf_hi = c->leaf_hi;
     s.cnt = (c->K == 1) ? c->pan_own_cnt.get() : c->quad_own_cnt.get();
@@ -178,7 +183,7 @@ TgtArg own_targets(fmmbem_ctx* c, bool quad) {
 
 enum : int {
   E_START = 0, E_UP0, E_UP1, E_AR0, E_AR1, E_M2L0, E_M2L1, E_DN1, E_P2P0, E_P2P1, E_L2P0, E_L2P1, E_AG0, E_AG1,
-  E_NEAR1, E_END
+  E_NEAR1, E_XG0, E_XG1, E_END
 };
 
 // One FMM (or direct) evaluation.  With c->overlap the near field (P2P, independent of every
@@ -202,7 +207,9 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
   }
   if (!direct) {
     rec(E_UP0, fs);
-    launch_upward(c, s, fs);
+    SrcArg sf = s;
+    if (s.x_far) sf.x = s.x_far;
+    launch_upward(c, sf, fs);
     rec(E_UP1, fs);
     if (distributed) {  // the multipoles this rank's interaction lists need (LET)
       rec(E_AR0, fs);
@@ -222,6 +229,11 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     rec(E_DN1, fs);
   }
   if (ovl) FMM_CUDA(cudaEventRecord(c->join, fs));
+  if (s.ag_src) {  // x slices of the other ranks for the near field, overlapped with the far chain
+    rec(E_XG0, st);
+    comm_allgatherv_f32(c, s.ag_src, const_cast<float*>(s.x), c->pan_offs, st, /*second=*/true);
+    rec(E_XG1, st);
+  }
   rec(E_P2P0, st);
   launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
   rec(E_P2P1, st);
@@ -235,6 +247,7 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
   }
   rec(E_L2P1, st);
   c->timed_comm = timing && distributed && !direct;
+  c->timed_xg = timing && s.ag_src != nullptr;
 }
 
 // y = op(x) on this rank's panels; x, y local slices (pointers are shifted so that the kernels'
@@ -388,7 +401,7 @@ void fill_timing(fmmbem_ctx* c, bool direct) {
   }
   T.p2p = el(E_P2P0, E_P2P1);
   T.near = el(E_L2P1, E_NEAR1);
-  if (c->timed_comm) T.comm = el(E_AR0, E_AR1) + el(E_AG0, E_AG1);
+  if (c->timed_comm) T.comm = el(E_AR0, E_AR1) + (c->timed_xg ? el(E_XG0, E_XG1) : el(E_AG0, E_AG1));
   T.total = el(E_AG0, E_NEAR1);  // wall time of the whole product (overlapped phases counted once)
   T.p2p_interactions = c->p2p_inter_kp;
   T.m2l_pairs = direct ? 0 : c->m2l_pairs_kp;

@@ -24,6 +24,7 @@ struct NcclApi {
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;  // optional
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -50,6 +51,7 @@ NcclApi& api() {
   a.getUniqueId = (decltype(a.getUniqueId))sym("ncclGetUniqueId");
   a.commInitRank = (decltype(a.commInitRank))sym("ncclCommInitRank");
   a.commDestroy = (decltype(a.commDestroy))sym("ncclCommDestroy");
+  a.commSplit = (decltype(a.commSplit))dlsym(a.h, "ncclCommSplit");
   a.allReduce = (decltype(a.allReduce))sym("ncclAllReduce");
   a.broadcast = (decltype(a.broadcast))sym("ncclBroadcast");
   a.send = (decltype(a.send))sym("ncclSend");
@@ -79,11 +81,17 @@ void comm_init(fmmbem_ctx* c, const void* id128) {
   ncclComm_t comm;
   check(api().commInitRank(&comm, c->opt.nranks, id, c->opt.rank), "ncclCommInitRank");
   c->comm = comm;
+  if (api().commSplit) {  // collective over comm: every rank takes this branch (same libnccl)
+    ncclComm_t c2 = nullptr;
+    check(api().commSplit(comm, 0, c->opt.rank, &c2, nullptr), "ncclCommSplit");
+    c->comm2 = c2;
+  }
 }
 
 void comm_destroy(fmmbem_ctx* c) {
+  if (c->comm2) api().commDestroy((ncclComm_t)c->comm2);
   if (c->comm) api().commDestroy((ncclComm_t)c->comm);
-  c->comm = nullptr;
+  c->comm = c->comm2 = nullptr;
 }
 
 void comm_allreduce_f32(fmmbem_ctx* c, float* buf, size_t n, cudaStream_t s) {
@@ -98,14 +106,15 @@ void comm_allreduce_f64(fmmbem_ctx* c, double* buf, size_t n, cudaStream_t s) {
 
 // full[offs[r] : offs[r+1]] <- rank r's slice, for every r (uneven slices: grouped broadcasts)
 void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const std::vector<int64_t>& offs,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool second) {
   const int R = c->opt.nranks;
+  const ncclComm_t cm = (ncclComm_t)(second && c->comm2 ? c->comm2 : c->comm);
   check(api().groupStart(), "ncclGroupStart");
   for (int r = 0; r < R; ++r) {
     const size_t n = (size_t)(offs[r + 1] - offs[r]);
     if (!n) continue;
     check(api().broadcast(r == c->opt.rank ? (const void*)mine : (const void*)(full + offs[r]), full + offs[r], n,
-                          ncclFloat32, r, (ncclComm_t)c->comm, s),
+                          ncclFloat32, r, cm, s),
           "ncclBroadcast");
   }
   check(api().groupEnd(), "ncclGroupEnd");

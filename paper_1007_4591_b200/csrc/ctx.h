@@ -118,7 +118,9 @@ struct fmmbem_ctx {
   int64_t m2l_pairs_kp = 0;
   // multi-GPU partition: this rank owns leaves [leaf_lo, leaf_hi) and the panels
   // [pan_lo, pan_hi) of the tree order; pan_offs[r] = first panel of rank r
-  void* comm = nullptr;  // ncclComm_t (nranks > 1)
+  void* comm = nullptr;   // ncclComm_t (nranks > 1)
+  void* comm2 = nullptr;  // second communicator (ncclCommSplit) for the x all-gather, so it can run
+                          // on the caller's stream concurrently with the multipole exchange
   int rank = 0, nranks = 1;
   int leaf_lo = 0, leaf_hi = 0;
   int64_t pan_lo = 0, pan_hi = 0;
@@ -131,9 +133,10 @@ struct fmmbem_ctx {
   int64_t n_own() const { return pan_hi - pan_lo; }
   fmmbem_timing last{};
   // phase events (E_* in api.cu); recorded on the stream that runs the phase
-  cudaEvent_t ev[16] = {};
-  cudaEvent_t fork = nullptr, join = nullptr;  // untimed fork/join of the P2P side stream
-  cudaStream_t side = nullptr;                 // P2P runs here when overlap is on
+  cudaEvent_t ev[20] = {};
+  cudaEvent_t fork = nullptr, join = nullptr;  // untimed fork/join of the far-field stream
+  cudaStream_t side = nullptr;                 // far-field chain runs here when overlap is on
   int overlap = 0;                             // 1: P2P concurrent with the upward/M2L/exchange chain
+  bool timed_xg = false;
   bool timed_comm = false, timed_near = false;
 };

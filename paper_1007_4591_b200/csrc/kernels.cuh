@@ -21,6 +21,8 @@ struct OutArg {
 struct SrcArg {
   const PointSet* set = nullptr;
   const float* x = nullptr;
+  const float* x_far = nullptr;  // weights for the upward sweep if different from x (owned slice view)
+  const float* ag_src = nullptr;  // deferred all-gather ag_src -> x (run by fmm_eval before P2P)
   int leaf_lo = 0, leaf_hi = -1;
   const int* cnt = nullptr;
 };
@@ -57,7 +59,7 @@ void comm_destroy(fmmbem_ctx* c);
 void comm_allreduce_f32(fmmbem_ctx* c, float* buf, size_t n, cudaStream_t s);
 void comm_allreduce_f64(fmmbem_ctx* c, double* buf, size_t n, cudaStream_t s);
 void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const std::vector<int64_t>& offs,
-                         cudaStream_t s);
+                         cudaStream_t s, bool second = false);
 void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds);
 void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std::vector<size_t>& scnt,
                        const std::vector<float*>& rbuf, const std::vector<size_t>& rcnt, cudaStream_t s);
