@@ -70,7 +70,9 @@ typedef struct {
                             P:415-418) for pairs |c_i - c_j| < near_radius*sqrt(A_j) and the single-layer
                             self term; default 0 */
   float near_radius;     /* eta of the near criterion; default 3; eta*sqrt(A) must stay below the leaf width */
-  int32_t self_term;     /* 0 only: K'_ii = 0 (flat panel) */
+  int32_t self_term;     /* 0: K'_ii = 0 (flat panel); 1: curvature term
+                            K'_ii = -H_i sqrt(A_i/pi)/4, H_i from area-weighted vertex normals
+                            (computed on the host at create, FP64) */
   int32_t direct;        /* 1 = bypass the FMM: all-pairs P2P (paper Fig. 11 "direct") */
   int32_t deterministic; /* reductions have a fixed order (no atomics on results); always true */
   int32_t device;        /* CUDA ordinal used by this ctx */

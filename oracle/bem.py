@@ -82,6 +82,7 @@ class Panels:
         self.qpts = (beta[None, :, 0, None] * v0[:, None, :] + beta[None, :, 1, None] * v1[:, None, :]
                      + beta[None, :, 2, None] * v2[:, None, :])
         self.n = len(t)
+        self._v, self._t = v, t  # kept for the curvature self-term option (vertex normals)
 
     # flattened quadrature sources: position, owner panel, weight factor A_j w_g
     def sources(self):
@@ -105,12 +106,44 @@ def normal_field(pan: Panels, cxyz, cq, eps_in: float):
     return _cdirect.dn_sum(pan.centroid, pan.normal, None, cxyz, cq, None) / eps_in
 
 
-def apply_kprime(pan: Panels, x, rows=None):
-    """O4: (K'x)_i = sum_{j!=i} x_j A_j sum_g w_g dG/dn_i(c_i, y_jg); K'_ii = 0 (P:326-327, S:364)."""
+def mean_curvature(pan: Panels):
+    """Per-panel mean curvature for the self_term = 1 option ("from vertex normals").
+
+    Vertex normal n_a = normalised sum of the incident faces' area-weighted normals.  The normal
+    curvature of the surface along the chord from the centroid c_i to vertex a is estimated by
+    (n_a - n_i).(v_a - c_i) / |v_a - c_i|^2 (on a sphere of radius R, n(v) = (v - o)/R makes this
+    1/R up to O(h)); the mean over the three chords estimates H_i.  Convex outward surface: H > 0.
+    """
+    v, t = pan._v, pan._t
+    acc = np.zeros_like(v)
+    for a in range(3):  # area-weighted face normals summed at each vertex
+        np.add.at(acc, t[:, a], pan.normal * pan.area[:, None])
+    nv = acc / np.linalg.norm(acc, axis=1)[:, None]
+    H = np.zeros(pan.n)
+    for a in range(3):
+        d = v[t[:, a]] - pan.centroid
+        H += np.einsum("ij,ij->i", nv[t[:, a]] - pan.normal, d) / np.einsum("ij,ij->i", d, d)
+    return H / 3.0
+
+
+def self_term_diag(pan: Panels):
+    """K'_ii = -H_i sqrt(A_i/pi) / 4: the principal-value integral of dG/dn_i over the
+    curved panel, modelled as a spherical cap of curvature H_i and area A_i.  On a sphere
+    dG/dn_x(x, y) = -1/(8 pi R |x - y|) for x, y on the surface, and the integral of 1/|x - y| over
+    a disc of radius a = sqrt(A/pi) is 2 pi a, giving -a/(4R)."""
+    return -mean_curvature(pan) * np.sqrt(pan.area / np.pi) / 4.0
+
+
+def apply_kprime(pan: Panels, x, rows=None, self_term: bool = False):
+    """O4: (K'x)_i = sum_{j!=i} x_j A_j sum_g w_g dG/dn_i(c_i, y_jg); K'_ii = 0 (P:326-327, S:364),
+    or K'_ii = self_term_diag (option self_term = 1)."""
     y, owner, aw = pan.sources()
     w = np.repeat(np.asarray(x, np.float64), pan.K) * aw
     idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)
-    return _cdirect.dn_sum(pan.centroid[idx], pan.normal[idx], idx, y, w, owner)
+    out = _cdirect.dn_sum(pan.centroid[idx], pan.normal[idx], idx, y, w, owner)
+    if self_term:
+        out = out + self_term_diag(pan)[idx] * np.asarray(x, np.float64)[idx]
+    return out
 
 
 def apply_single(pan: Panels, x, rows=None):
@@ -171,9 +204,9 @@ def apply_single_near(pan: Panels, x, eta: float = 3.0):
     return apply_single(pan, x) + np.bincount(i, weights=c_pot * x[j], minlength=pan.n) + self_pot * x
 
 
-def apply_A(pan: Panels, x, f: float):
+def apply_A(pan: Panels, x, f: float, self_term: bool = False):
     """GMRES operator (I - f K') x  ("A x = B q")."""
-    return np.asarray(x, np.float64) - f * apply_kprime(pan, x)
+    return np.asarray(x, np.float64) - f * apply_kprime(pan, x, self_term=self_term)
 
 
 def reaction_potential(pan: Panels, sigma, cxyz):
@@ -189,7 +222,7 @@ def solvation_energy(cq, phi_reac):
     return e, e * KCAL_PER_INTERNAL
 
 
-def dense_kprime(pan: Panels):
+def dense_kprime(pan: Panels, self_term: bool = False):
     """Dense K' (n_p <= ~10^4): column j = K' e_j, assembled entry by entry as in O4."""
     n = pan.n
     c, nr = pan.centroid, pan.normal
@@ -203,12 +236,14 @@ def dense_kprime(pan: Panels):
         blk = -nd / (4.0 * np.pi * r2 * np.sqrt(r2)) * (pan.area * pan.wq[g])[None, :]
         np.fill_diagonal(blk, 0.0)
         Kp += blk
+    if self_term:
+        Kp[np.diag_indices(n)] = self_term_diag(pan)
     return Kp
 
 
-def solve_dense(pan: Panels, E, f: float):
+def solve_dense(pan: Panels, E, f: float, self_term: bool = False):
     """O6 (direct): (I - f K') sigma = f E by dense LU."""
-    A = np.eye(pan.n) - f * dense_kprime(pan)
+    A = np.eye(pan.n) - f * dense_kprime(pan, self_term)
     return np.linalg.solve(A, f * np.asarray(E))
 
 
@@ -284,9 +319,10 @@ BIBEE_SCALE = {"cfa": -0.5, "p": 0.0, "lb": 0.5}
 class Problem:
     """A molecule: mesh + charges + dielectrics; the full oracle pipeline (O1-O9)."""
 
-    def __init__(self, cfg, K: int = 1, near_eta=None):
+    def __init__(self, cfg, K: int = 1, near_eta=None, self_term: bool = False):
         self.pan = Panels(cfg["vertices"], cfg["triangles"], K)
         self.near_eta = near_eta  # None: paper's quadrature only; else the analytic near-field option
+        self.self_term = self_term  # True: curvature self-term K'_ii (option self_term = 1, A7)
         self.cxyz = np.asarray(cfg["charge_xyz"], np.float64).reshape(-1, 3)
         self.cq = np.asarray(cfg["charge_q"], np.float64).reshape(-1)
         self.eps_in, self.eps_out = float(cfg["eps_in"]), float(cfg["eps_out"])
@@ -304,11 +340,11 @@ class Problem:
 
     def solve(self, method="dense", tol=1e-6, restart=30, max_iters=200):
         if method == "dense":
-            sigma = solve_dense(self.pan, self.E, self.f)
+            sigma = solve_dense(self.pan, self.E, self.f, self.self_term)
             info = dict(iterations=0, converged=True)
         else:
             if self.near_eta is None:
-                op = lambda v: apply_A(self.pan, v, self.f)  # noqa: E731
+                op = lambda v: apply_A(self.pan, v, self.f, self.self_term)  # noqa: E731
             else:
                 op = lambda v: np.asarray(v) - self.f * apply_kprime_near(self.pan, v, self.near_eta)  # noqa: E731
             sigma, its, hist, conv = gmres(op, self.f * self.E, tol, restart, max_iters)

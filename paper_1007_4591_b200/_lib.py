@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfmmbem.so")
+LIB_PATH = os.environ.get("FMMBEM_LIB") or os.path.join(HERE, "libfmmbem.so")  # override: A/B builds
 
 OK, NOT_CONVERGED = 0, 1
 E_INVALID, E_DEGENERATE, E_COINCIDENT, E_CUDA, E_NOMEM, E_NCCL = -1, -2, -3, -4, -5, -6

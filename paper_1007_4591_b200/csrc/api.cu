@@ -186,6 +186,58 @@ enum : int {
   E_NEAR1, E_XG0, E_XG1, E_END
 };
 
+// Option self_term = 1: K'_ii = -H_i sqrt(A_i / pi) / 4, the principal-value integral of
+// dG/dn_i over panel i modelled as a spherical cap of mean curvature H_i.  H_i from the mesh in
+// FP64 on the host: vertex normals = normalised sums of the incident faces' area-weighted normals;
+// the normal curvature along the chord centroid -> vertex a is (n_a - n_i).(v_a - c_i)/|v_a - c_i|^2,
+// and H_i is the mean over the three vertices.  Stored in local order, times 4 pi (the kernels
+// sum raw 1/r^3 terms and apply 1/(4 pi) in the epilogue).
+void build_self_term(fmmbem_ctx* c, const fmmbem_mesh* mesh, cudaStream_t s) {
+  const int64_t nv = mesh->n_vertices, np = mesh->n_triangles;
+  const double* V = mesh->xyz;
+  const int* T = mesh->tri;
+  std::vector<double> vn(3 * nv, 0.0), fn(3 * np), cen(3 * np), area(np);
+  for (int64_t t = 0; t < np; ++t) {
+    const double* a = V + 3 * T[3 * t];
+    const double* b = V + 3 * T[3 * t + 1];
+    const double* q = V + 3 * T[3 * t + 2];
+    const double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]}, e2[3] = {q[0] - a[0], q[1] - a[1], q[2] - a[2]};
+    const double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const double len = std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+    area[t] = 0.5 * len;
+    for (int d = 0; d < 3; ++d) {
+      fn[3 * t + d] = cr[d] / len;
+      cen[3 * t + d] = (a[d] + b[d] + q[d]) / 3.0;
+      for (int k = 0; k < 3; ++k) vn[3 * T[3 * t + k] + d] += 0.5 * cr[d];  // area-weighted face normal
+    }
+  }
+  for (int64_t v = 0; v < nv; ++v) {
+    const double l = std::sqrt(vn[3 * v] * vn[3 * v] + vn[3 * v + 1] * vn[3 * v + 1] + vn[3 * v + 2] * vn[3 * v + 2]);
+    if (l > 0)
+      for (int d = 0; d < 3; ++d) vn[3 * v + d] /= l;
+  }
+  std::vector<float> dl(np);
+  for (int64_t k = 0; k < np; ++k) {
+    const int64_t t = c->pan_ids[k];
+    double H = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      const int64_t v = T[3 * t + j];
+      double num = 0.0, den = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        const double ch = V[3 * v + d] - cen[3 * t + d];
+        num += (vn[3 * v + d] - fn[3 * t + d]) * ch;
+        den += ch * ch;
+      }
+      H += num / den;
+    }
+    H /= 3.0;
+    dl[k] = (float)(-H * std::sqrt(area[t] / M_PI) / 4.0 * 4.0 * M_PI);
+  }
+  c->selfd.alloc(np);
+  FMM_CUDA(cudaMemcpyAsync(c->selfd.get(), dl.data(), np * sizeof(float), cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
 // One FMM (or direct) evaluation.  With c->overlap the near field (P2P, independent of every
 // expansion) runs on a side stream concurrently with the upward sweep, the multipole exchange and
 // M2L/L2L; L2P then waits for it (y is first written by P2P, L2P accumulates).
@@ -268,6 +320,10 @@ void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_
       o.dn.x = xg;
       o.dn.ax = 1.f;
       o.dn.b = (float)(-c->f / FOUR_PI);
+    }
+    if (c->selfd.n) {  // K'_ii = d_i (stored times 4 pi, like the raw kernel sums)
+      o.dn.x = xg;
+      o.dn.d = c->selfd.get();
     }
   }
   bool dist = false;
@@ -464,7 +520,7 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
     throw Error(FMMBEM_E_INVALID, "quad_points must be 1, 3, 6 or 7");
   if (opt.near_mode != 0 && opt.near_mode != 1) throw Error(FMMBEM_E_INVALID, "near_mode must be 0 or 1");
   if (opt.near_mode == 1 && !(opt.near_radius > 0.f)) throw Error(FMMBEM_E_INVALID, "near_radius must be > 0");
-  if (opt.self_term != 0) throw Error(FMMBEM_E_INVALID, "self_term = 1 is not available yet");
+  if (opt.self_term != 0 && opt.self_term != 1) throw Error(FMMBEM_E_INVALID, "self_term must be 0 or 1");
   if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks) throw Error(FMMBEM_E_INVALID, "bad rank / nranks");
   if (opt.nranks > 1 && !opt.nccl_id) throw Error(FMMBEM_E_INVALID, "nranks > 1 needs options.nccl_id");
   if (opt.nranks > 1 && opt.direct) throw Error(FMMBEM_E_INVALID, "direct mode is single-GPU only");
@@ -581,6 +637,7 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
     if (!(c->opt.direct != 0 || c->tree.L < 2) && !(e && std::atoi(e) == 0)) build_let(c, c->leaf_bounds, s);
   }
   if (c->opt.near_mode == 1) build_near(c, dV.get(), dT.get(), cen.get(), nrm.get(), area.get(), beta.get(), wq.get(), s);
+  if (c->opt.self_term == 1) build_self_term(c, mesh, s);
   dV.release();
   dT.release();
   c->m2l_pairs_kp = 0;

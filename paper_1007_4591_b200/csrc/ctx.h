@@ -127,6 +127,7 @@ struct fmmbem_ctx {
   std::vector<int64_t> pan_offs;
   fmm::DevBuf<int> pan_own_cnt, quad_own_cnt;  // subtree counts of owned points
   fmm::DevBuf<float> xfull;                    // all-gathered source weights
+  fmm::DevBuf<float> selfd;                    // [np] curvature self-term K'_ii in local order (self_term = 1)
   fmm::NearCSR near;                           // near_mode = 1 corrections
   fmm::LetPlan let;                            // multipole LET exchange plan (nranks > 1)
   std::vector<int64_t> leaf_bounds;            // [nranks + 1] leaf partition

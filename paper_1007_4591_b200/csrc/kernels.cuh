@@ -12,6 +12,7 @@ struct OutArg {
   const float* x = nullptr;
   float ax = 0.f;
   float b = 1.f;
+  const float* d = nullptr;  // optional diagonal: y_i += b d_i x_i (curvature self-term, option self_term)
 };
 
 // A source set for one apply: weight of point j = (x ? x[j / div] : 1) * pos[j].w

@@ -26,7 +26,7 @@ namespace fmm {
 
 namespace {
 
-constexpr int TILE = 128;   // sources per warp tile
+constexpr int TILE = 256;   // sources per warp tile (256 and unroll 8 measured ~2% faster than 128 / 4)
 constexpr int MAXSEG = 32;
 
 struct P2PArgs {
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
     const int mlo = SELF ? min(max(self_lo - base, 0), tcnt) : tcnt;
     const int mhi = SELF ? min(max(self_hi - base, 0), tcnt) : tcnt;
     // unmasked: [0, mlo) and [mhi, tcnt)
-#pragma unroll 4
+#pragma unroll 8
     for (int k = sub; k < mlo; k += step) {
       const float4 sv = tile[k];
 #pragma unroll
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
     }
     if (SELF) {
       int k0 = mhi + ((sub - mhi) % S + S) % S;
-#pragma unroll 4
+#pragma unroll 8
       for (int k = k0; k < tcnt; k += step) {
         const float4 sv = tile[k];
 #pragma unroll
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
       if (DN) {
         const float4 n = a.tnrm[i];
         float v = a.dn.b * fmaf(n.x, gx[q], fmaf(n.y, gy[q], n.z * gz[q]));
-        if (a.dn.x) v = fmaf(a.dn.ax, a.dn.x[i], v);
+        if (a.dn.x) v = fmaf(a.dn.d ? fmaf(a.dn.b, a.dn.d[i], a.dn.ax) : a.dn.ax, a.dn.x[i], v);
         a.dn.y[i] = v;
       }
     }

@@ -240,3 +240,35 @@ def test_near_mode_solve_energy():
     r = s.solve()
     ref = bem.Problem(cfg, near_eta=3.0).solve("gmres")
     assert abs(r["dG"] / ref["dG"] - 1) < 1e-3, (r["dG"], ref["dG"])
+
+
+@pytest.mark.parametrize("op", ["kprime", "A"])
+def test_self_term_matches_oracle(problems, op):
+    """Option self_term = 1: the curvature diagonal K'_ii computed on the host in C++
+    from the mesh agrees with the oracle's (independent numpy) through the whole operator."""
+    cfg, P = problems["lyso20"]
+    x = np.random.default_rng(14).normal(size=P.pan.n)
+    if op == "kprime":
+        ref = bem.apply_kprime(P.pan, x, self_term=True)
+    else:
+        ref = bem.apply_A(P.pan, x, P.f, self_term=True)
+    assert bem.rel_l2(ref, ref_op(P, x, op)) > 1e-3  # the diagonal is visible
+    for direct, tol in ((1, 2e-5), (0, 1e-4)):
+        s = solver(cfg, self_term=1, direct=direct, terms=12, leaf_points=16)
+        err = bem.rel_l2(run(s, x, op), ref)
+        assert err < tol, (direct, err)
+
+
+def test_self_term_born_energy():
+    """Born ion with the curvature self-term: GPU GMRES energy equals the oracle's dense solve
+    (1e-5, the Born pin's tolerance) and is 1.7 % from the continuum."""
+    cfg = configs.born(8)
+    ref = bem.Problem(cfg, self_term=True).solve("dense")["dG"]
+    r = solver(cfg, self_term=1, direct=1).solve()
+    assert abs(r["dG"] / ref - 1) < 1e-5
+    assert abs(r["dG"] / closed_born() - 1) == pytest.approx(0.0170, abs=5e-4)
+
+
+def closed_born():
+    from oracle import closed_forms
+    return closed_forms.born(1.0, 1.0, 4.0, 80.0)
