@@ -1,0 +1,15 @@
+#!/bin/bash
+# Round-end measurement on one B200: GPU tests, the bench line, the reference arm, the ncu launch
+# list of the bench command (after the same command exited 0 without ncu) and a full ncu capture of
+# the per-matvec kernels.  Outputs land in gpurun_out/ and are summarised into profiles/.
+python -m pytest tests -m gpu -q 2>&1 | tail -3
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -1 gpurun_out/bench_final.json
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -1 gpurun_out/bench_ref.json
+python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/b_plain.json 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+      python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
+python tools/prof_run.py --reps 2 > gpurun_out/prof_plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on \
+      -k regex:"k_p2p|k_m2l_rot|k_m2m_rot|k_l2l_rot|k_p2m_t|k_l2p_t|k_m2m_sum" -s 22 -c 22 \
+      -o gpurun_out/prof_final python tools/prof_run.py --reps 2 > gpurun_out/ncu_full_final.log 2>&1
+tail -2 gpurun_out/ncu_full_final.log
