@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libfmmbem (include/fmmbem.h) and the orchestration of one FMM
 // evaluation.  Every step of the path runs in this library's kernels;
 // the host only validates, launches and runs the small FP64 GMRES least-squares problem.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -304,6 +305,28 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
 
 // y = op(x) on this rank's panels; x, y local slices (pointers are shifted so that the kernels'
 // global tree indices land in the slice)
+Outputs op_outputs(fmmbem_ctx* c, fmmbem_op op, const float* xg, float* yg) {
+  Outputs o;
+  if (op == FMMBEM_OP_SINGLE) {
+    o.pot.y = yg;
+    o.pot.b = (float)(1.0 / FOUR_PI);
+  } else {
+    o.dn.y = yg;
+    if (op == FMMBEM_OP_KPRIME) {
+      o.dn.b = (float)(1.0 / FOUR_PI);
+    } else {  // A = I - f K'
+      o.dn.x = xg;
+      o.dn.ax = 1.f;
+      o.dn.b = (float)(-c->f / FOUR_PI);
+    }
+    if (c->selfd.n) {  // K'_ii = d_i (stored times 4 pi, like the raw kernel sums)
+      o.dn.x = xg;
+      o.dn.d = c->selfd.get();
+    }
+  }
+  return o;
+}
+
 void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_t st, bool timing) {
   TgtArg t = own_targets(c, false);
   float* yg = y - c->pan_lo;
@@ -674,6 +697,10 @@ void fmmbem_destroy(fmmbem_ctx* c) {
     if (c->side) cudaStreamSynchronize(c->side);
     for (auto& e : c->ev)
       if (e) cudaEventDestroy(e);
+    if (c->cstream) {
+      cudaStreamDestroy(c->cstream);
+      for (auto& e : c->pev) cudaEventDestroy(e);
+    }
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
     if (c->side) cudaStreamDestroy(c->side);
@@ -717,14 +744,95 @@ fmmbem_status fmmbem_matvec(fmmbem_ctx* c, fmmbem_op op, const float* x, float* 
   API_END
 }
 
+// Host-buffer matvec with the transfers pipelined against the kernels (single GPU, K = 1, no
+// near-field option): x arrives in NCH Morton-contiguous chunks on a copy stream and P2M of each
+// chunk's leaves starts as soon as it lands; the far field runs next and L2P writes y first; P2P
+// then adds the near field chunk by chunk and each chunk of y leaves for the host while the next
+// chunk computes.  Same operations as apply_op (P2P and L2P swap order; P2P accumulates).
+void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* yh) {
+  constexpr int NCH = 4;
+  cudaStream_t st = c->stream;
+  const Tree& T = c->tree;
+  const int64_t np = c->np;
+  if (c->h_pan_begin.empty()) {
+    c->h_pan_begin.resize(T.n_leaves + 1);
+    FMM_CUDA(cudaMemcpy(c->h_pan_begin.data(), c->pan.begin.get(), (T.n_leaves + 1) * sizeof(int),
+                        cudaMemcpyDeviceToHost));
+  }
+  if (!c->cstream) {
+    FMM_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (auto& e : c->pev) FMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int lb[NCH + 1];
+  lb[0] = 0;
+  for (int k = 1; k < NCH; ++k) {
+    const int64_t goal = np * k / NCH;
+    lb[k] = (int)(std::lower_bound(c->h_pan_begin.begin(), c->h_pan_begin.end(), (int)goal) - c->h_pan_begin.begin());
+    lb[k] = std::max(lb[k - 1], std::min(lb[k], (int)T.n_leaves));
+  }
+  lb[NCH] = (int)T.n_leaves;
+  float* x = c->tmp_x.get();
+  float* y = c->tmp_y.get();
+  cudaEvent_t* eh = c->pev;            // x chunk k on the device
+  cudaEvent_t* ep = c->pev + NCH;      // y chunk k final
+  cudaEvent_t e0 = c->pev[2 * NCH];    // previous work on st done with tmp_x / tmp_y
+  FMM_CUDA(cudaEventRecord(e0, st));
+  FMM_CUDA(cudaStreamWaitEvent(c->cstream, e0, 0));
+  for (int k = 0; k < NCH; ++k) {
+    const int64_t p0 = c->h_pan_begin[lb[k]], p1 = c->h_pan_begin[lb[k + 1]];
+    if (p1 > p0)
+      FMM_CUDA(cudaMemcpyAsync(x + p0, xh + p0, (p1 - p0) * sizeof(float), cudaMemcpyHostToDevice, c->cstream));
+    FMM_CUDA(cudaEventRecord(eh[k], c->cstream));
+  }
+  SrcArg s;
+  s.set = &c->pan;
+  s.x = x;
+  c->Mx.zero(st);
+  for (int k = 0; k < NCH; ++k) {
+    FMM_CUDA(cudaStreamWaitEvent(st, eh[k], 0));
+    launch_p2m_range(c, s, lb[k], lb[k + 1], st);
+  }
+  launch_m2m_levels(c, s, st);
+  launch_m2l(c, c->pan.cell_cnt.get(), c->pan.cell_cnt.get(), st);
+  launch_downward(c, c->pan.cell_cnt.get(), st);
+  Outputs o = op_outputs(c, op, x, y);
+  FMM_CUDA(cudaMemsetAsync(y, 0, np * sizeof(float), st));
+  TgtArg t = own_targets(c, false);
+  Outputs far = o;
+  far.pot.x = far.dn.x = nullptr;
+  far.pot.d = far.dn.d = nullptr;
+  launch_l2p(c, t, far, st);
+  o.pot.acc = o.dn.acc = 1;
+  for (int k = 0; k < NCH; ++k) {
+    TgtArg tk = t;
+    tk.leaf_lo = lb[k];
+    tk.leaf_hi = lb[k + 1];
+    launch_p2p(c, tk, s, o, /*self=*/true, /*check=*/false, /*direct=*/false, st);
+    FMM_CUDA(cudaEventRecord(ep[k], st));
+    FMM_CUDA(cudaStreamWaitEvent(c->cstream, ep[k], 0));
+    const int64_t p0 = c->h_pan_begin[lb[k]], p1 = c->h_pan_begin[lb[k + 1]];
+    if (p1 > p0)
+      FMM_CUDA(cudaMemcpyAsync(yh + p0, y + p0, (p1 - p0) * sizeof(float), cudaMemcpyDeviceToHost, c->cstream));
+  }
+  FMM_CUDA(cudaStreamSynchronize(c->cstream));
+  FMM_CUDA(cudaStreamSynchronize(st));
+}
+
 fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* yh) {
   API_BEGIN
   if (!c || !xh || !yh) throw Error(FMMBEM_E_INVALID, "matvec_host: null vectors");
+  if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_A) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
   DevGuard dg(c->device);
   cudaStream_t st = c->stream;
   const int64_t n = c->n_own();
   c->tmp_x.alloc(std::max<int64_t>(n, 1));
   c->tmp_y.alloc(std::max<int64_t>(n, 1));
+  const bool pipelined = c->nranks == 1 && c->K == 1 && c->opt.near_mode == 0 && c->opt.direct == 0 &&
+                         c->tree.L >= 2 && std::getenv("FMMBEM_E2E_PLAIN") == nullptr;
+  if (pipelined) {
+    matvec_host_pipelined(c, op, xh, yh);
+    return FMMBEM_OK;
+  }
   FMM_CUDA(cudaMemcpyAsync(c->tmp_x.get(), xh, n * sizeof(float), cudaMemcpyHostToDevice, st));
   apply_op(c, op, c->tmp_x.get(), c->tmp_y.get(), st, true);
   FMM_CUDA(cudaMemcpyAsync(yh, c->tmp_y.get(), n * sizeof(float), cudaMemcpyDeviceToHost, st));

@@ -419,24 +419,34 @@ void init_tables(fmmbem_ctx* c) {
   c->NI = NIF;
 }
 
+void launch_p2m_range(fmmbem_ctx* c, const SrcArg& s, int lo, int hi, cudaStream_t st) {
+  const Tree& T = c->tree;
+  const int L = T.L, P = c->P;
+  if (L < 2 || hi <= lo) return;
+  const PointSet& S = *s.set;
+  if (exp_specialised(P)) {
+    launch_p2m_t(P, hi - lo, S.pos.get(), s.x, S.div, S.begin.get(), (float)(1.0 / T.width(L)), (int)T.lvl_off[L],
+                 lo, c->Mx.get(), st);
+  } else {
+    k_p2m<<<hi - lo, 128, 0, st>>>(S.pos.get(), s.x, S.div, S.begin.get(), P, (float)(1.0 / T.width(L)),
+                                   (int)T.lvl_off[L], lo, c->Mx.get());
+    FMM_CHECK_LAUNCH();
+  }
+}
+
 void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
+  const Tree& T = c->tree;
+  if (T.L < 2) return;
+  c->Mx.zero(st);
+  launch_p2m_range(c, s, s.leaf_lo, s.leaf_hi < 0 ? (int)T.n_leaves : s.leaf_hi, st);
+  launch_m2m_levels(c, s, st);
+}
+
+void launch_m2m_levels(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
   const Tree& T = c->tree;
   const int L = T.L, P = c->P, NC = c->NC;
   if (L < 2) return;
-  c->Mx.zero(st);
-  const PointSet& S = *s.set;
-  const int lo = s.leaf_lo, hi = s.leaf_hi < 0 ? (int)T.n_leaves : s.leaf_hi;
-  const int* cnt = s.cnt ? s.cnt : S.cell_cnt.get();
-  if (hi > lo) {
-    if (exp_specialised(P)) {
-      launch_p2m_t(P, hi - lo, S.pos.get(), s.x, S.div, S.begin.get(), (float)(1.0 / T.width(L)),
-                   (int)T.lvl_off[L], lo, c->Mx.get(), st);
-    } else {
-      k_p2m<<<hi - lo, 128, 0, st>>>(S.pos.get(), s.x, S.div, S.begin.get(), P, (float)(1.0 / T.width(L)),
-                                     (int)T.lvl_off[L], lo, c->Mx.get());
-      FMM_CHECK_LAUNCH();
-    }
-  }
+  const int* cnt = s.cnt ? s.cnt : s.set->cell_cnt.get();
   const bool rot = c->m2l_mode == 0 && m2m_rot_supported(P);
   if (rot) init_rot_tables();
   for (int l = L - 1; l >= 2; --l) {

@@ -13,6 +13,7 @@ struct OutArg {
   float ax = 0.f;
   float b = 1.f;
   const float* d = nullptr;  // optional diagonal: y_i += b d_i x_i (curvature self-term, option self_term)
+  int acc = 0;               // P2P: add to y instead of overwriting it (far field written first)
 };
 
 // A source set for one apply: weight of point j = (x ? x[j / div] : 1) * pos[j].w
@@ -71,6 +72,9 @@ int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self
 
 // far field (expansions in c->Mx / c->Lx); l2p accumulates y += b far
 void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
+// the two halves of launch_upward: P2M over leaves [lo, hi) (Mx must be zeroed first), then M2M
+void launch_p2m_range(fmmbem_ctx* c, const SrcArg& s, int lo, int hi, cudaStream_t st);
+void launch_m2m_levels(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
 void launch_m2l(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStream_t st);
 void launch_downward(fmmbem_ctx* c, const int* tgt_cnt, cudaStream_t st);
 void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t st);

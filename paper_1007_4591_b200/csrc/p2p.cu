@@ -266,12 +266,14 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
       if (POT) {
         float v = a.pot.b * ap[q];
         if (a.pot.x) v = fmaf(a.pot.ax, a.pot.x[i], v);
+        if (a.pot.acc) v = __fadd_rn(v, a.pot.y[i]);
         a.pot.y[i] = v;
       }
       if (DN) {
         const float4 n = a.tnrm[i];
         float v = a.dn.b * fmaf(n.x, gx[q], fmaf(n.y, gy[q], n.z * gz[q]));
         if (a.dn.x) v = fmaf(a.dn.d ? fmaf(a.dn.b, a.dn.d[i], a.dn.ax) : a.dn.ax, a.dn.x[i], v);
+        if (a.dn.acc) v = __fadd_rn(v, a.dn.y[i]);
         a.dn.y[i] = v;
       }
     }

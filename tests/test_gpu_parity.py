@@ -272,3 +272,18 @@ def test_self_term_born_energy():
 def closed_born():
     from oracle import closed_forms
     return closed_forms.born(1.0, 1.0, 4.0, 80.0)
+
+
+@pytest.mark.parametrize("op", ["kprime", "A", "single"])
+def test_host_buffer_matvec_equals_device_matvec(problems, op):
+    """fmmbem_matvec_host (pipelined transfers: P2P after L2P, chunked) computes the device product:
+    the same near and far partial sums per panel, combined in the other order -- equal up to the
+    rounding of that one addition (FMA contraction differs), i.e. to FP32 epsilon."""
+    cfg, P = problems["lyso20"]
+    s = solver(cfg, terms=12, leaf_points=16)
+    x = np.random.default_rng(15).normal(size=s.n).astype(np.float32)
+    yd = s.matvec(torch.tensor(x, device="cuda"), op).cpu().numpy()
+    xp = torch.tensor(x).pin_memory()
+    yp = torch.empty_like(xp).pin_memory()
+    yh = s.matvec_host(xp.numpy(), op, y_host=yp.numpy())
+    assert bem.rel_l2(yh.astype(np.float64), yd.astype(np.float64)) < 1e-6

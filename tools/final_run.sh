@@ -11,5 +11,12 @@ python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/b_plain.json 2>&1 && 
 python tools/prof_run.py --reps 2 > gpurun_out/prof_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on \
       -k regex:"k_p2p|k_m2l_rot|k_m2m_rot|k_l2l_rot|k_p2m_t|k_l2p_t|k_m2m_sum" -s 22 -c 22 \
-      -o gpurun_out/prof_final python tools/prof_run.py --reps 2 > gpurun_out/ncu_full_final.log 2>&1
+      -o /tmp/prof_final python tools/prof_run.py --reps 2 > gpurun_out/ncu_full_final.log 2>&1
 tail -2 gpurun_out/ncu_full_final.log
+# the report itself stays on the box (gpurun_out must stay under 64 MiB): summaries only
+python tools/ncu_summary.py /tmp/prof_final.ncu-rep gpurun_out/ncu_full_final_summary.csv
+ncu -i /tmp/prof_final.ncu-rep --page raw --csv > gpurun_out/ncu_full_final_raw.csv 2>/dev/null
+for k in k_p2p k_m2l_rot; do
+  ncu -i /tmp/prof_final.ncu-rep --page source --csv --print-source sass -k regex:$k > gpurun_out/ncu_src_$k.csv 2>/dev/null
+done
+ls -la gpurun_out/
