@@ -1,5 +1,6 @@
 """Multi-GPU parity: the octree domain decomposition over NCCL reproduces the
-single-GPU matvec, GMRES solve and BIBEE energy.  Needs >= 2 GPUs (skipped otherwise)."""
+single-GPU matvec (also with the curvature self-term), GMRES solve and BIBEE energy, and the
+host-buffer product equals the device one.  Needs >= 2 GPUs (skipped otherwise)."""
 import json
 import os
 import subprocess
@@ -23,6 +24,8 @@ def test_two_gpus_match_one(case):
     assert line, out.stdout[-2000:] + out.stderr[-2000:]
     r = json.loads(line[0][5:])
     assert r["matvec_rel"] < 1e-6
+    assert r["self_term_rel"] < 1e-6  # option self_term = 1 on the domain decomposition
+    assert r["host_rel"] == 0.0  # host-buffer product = device product (same path on N > 1)
     g, o, gi, oi = r["solve"]
     assert abs(g / o - 1) < 1e-6 and abs(gi - oi) <= 1
     assert abs(r["bibee"][0] / r["bibee"][1] - 1) < 1e-6
