@@ -117,6 +117,7 @@ struct fmmbem_ctx {
   std::vector<std::unique_ptr<fmm::P2PItems>> p2p_cache;
   int m2l_mode = 0;  // 0 = rotation O(P^3) when available, 1 = plain O(P^4)
   int p2p_chunk = 64;   // P2P targets per work item (FMMBEM_P2P_CHUNK)
+  int p2p_scaled = 1;   // scaled-coordinate K' P2P (FMMBEM_P2P_PLAIN=1 -> plain form)
   int64_t p2p_inter_kp = 0, p2p_inter_chg = 0;  // exact interaction counts
   int64_t m2l_pairs_kp = 0;
   // multi-GPU partition: this rank owns leaves [leaf_lo, leaf_hi) and the panels

@@ -3,9 +3,9 @@
 // in the adjacent cells", "P2P ... the largest fractions").
 //
 // Work unit = one warp = one chunk of <= 64 targets of one leaf (T = 4 targets per lane in
-// registers as two packed FP32x2 pairs; measured at C5: T = 8 or 128-target chunks are slower --
-// registers -- and so is a scaled-coordinate form with one FP32x2 op fewer per interaction: the
-// loop is latency-, not issue-bound).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
+// registers as two packed FP32x2 pairs; measured at C5: T = 6 / 8 or 128-target chunks are slower).
+// The normal-derivative sums (K', A) use the scaled-coordinate form (interact2s, 11 instead of 12
+// packed instructions per pair of interactions, -2.8 % at C5).  Surface leaves hold a variable number of targets, so a leaf is cut into chunks
 // and a tail chunk with few targets spreads its lanes over S source subsets (split-K, reduced in
 // shared memory) -- lanes stay busy whatever the occupancy.  The sources of the (<= 27)
 // neighbour leaves stream through a warp-private shared-memory tile, already shifted into the
@@ -80,8 +80,30 @@ __device__ __forceinline__ void interact2(const float4 s, float2 px, float2 py, 
   }
 }
 
-template <int T, bool POT, bool DN, bool SELF, bool CHECK>
+// Scaled form for the normal-derivative-only sum (the K' / A matvec): the tile holds (a s, a) with
+// a = sign(w) |w|^(-1/2), so d' = a (s - x) = fma(a, -x, a s), r'^2 = a^2 r^2 and
+// (r'^-2)^(3/2) d' = sign(w) d / (a^2 r^3) = w d / r^3: 11 packed FP32x2 instructions + 2 MUFU.RSQ
+// per 2 interactions (12 in the plain form).  A zero weight becomes a source at 1e18 with a = 1
+// (its r'^-3 flushes to zero).  a comes from MUFU.RSQ: relative error ~2^-22 per source weight.
+template <bool MASK>
+__device__ __forceinline__ void interact2s(const float4 s, float2 px, float2 py, float2 pz, float2& gx, float2& gy,
+                                           float2& gz, bool skipa, bool skipb) {
+  const float2 dx = __ffma2_rn(bc2(s.w), px, bc2(s.x)), dy = __ffma2_rn(bc2(s.w), py, bc2(s.y)),
+               dz = __ffma2_rn(bc2(s.w), pz, bc2(s.z));
+  float2 r2 = __fmul2_rn(dx, dx);
+  r2 = __ffma2_rn(dy, dy, r2);
+  r2 = __ffma2_rn(dz, dz, r2);
+  float2 ri = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+  if (MASK) ri = make_float2(skipa ? 0.f : ri.x, skipb ? 0.f : ri.y);
+  const float2 t = __fmul2_rn(__fmul2_rn(ri, ri), ri);
+  gx = __ffma2_rn(t, dx, gx);
+  gy = __ffma2_rn(t, dy, gy);
+  gz = __ffma2_rn(t, dz, gz);
+}
+
+template <int T, bool POT, bool DN, bool SELF, bool CHECK, bool SC = false>
 __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
+  static_assert(!SC || (DN && !POT && !CHECK), "scaled form: normal derivative only");
   __shared__ float4 tile[TILE];
   __shared__ int own[SELF ? TILE : 1];
   __shared__ int seg_src[MAXSEG], seg_cum[MAXSEG + 1];
@@ -190,7 +212,16 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
         const float4 p = __ldg(a.spos + j);
         float w = p.w;
         if (a.sx) w *= __ldg(a.sx + (a.sdiv == 1 ? j : j / a.sdiv));
-        tile[k] = make_float4(p.x + sx, p.y + sy, p.z + sz, w);
+        if (SC) {
+          if (w == 0.f) {
+            tile[k] = make_float4(1e18f, 1e18f, 1e18f, 1.f);
+          } else {
+            const float sc = copysignf(rsqrtf(fabsf(w)), w);
+            tile[k] = make_float4(sc * (p.x + sx), sc * (p.y + sy), sc * (p.z + sz), sc);
+          }
+        } else {
+          tile[k] = make_float4(p.x + sx, p.y + sy, p.z + sz, w);
+        }
         if (SELF) own[k] = (a.sdiv == 1) ? j : j / a.sdiv;
       }
     }
@@ -203,9 +234,11 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
     for (int k = sub; k < mlo; k += step) {
       const float4 sv = tile[k];
 #pragma unroll
-      for (int q = 0; q < NP; ++q)
-        interact2<POT, DN, false, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], false, false,
-                                         a.flag);
+      for (int q = 0; q < NP; ++q) {
+        if (SC) interact2s<false>(sv, px[q], py[q], pz[q], gx2[q], gy2[q], gz2[q], false, false);
+        else interact2<POT, DN, false, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], false, false,
+                                              a.flag);
+      }
     }
     if (SELF) {
       int k0 = mhi + ((sub - mhi) % S + S) % S;
@@ -213,18 +246,22 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
       for (int k = k0; k < tcnt; k += step) {
         const float4 sv = tile[k];
 #pragma unroll
-        for (int q = 0; q < NP; ++q)
-          interact2<POT, DN, false, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], false, false,
-                                           a.flag);
+        for (int q = 0; q < NP; ++q) {
+          if (SC) interact2s<false>(sv, px[q], py[q], pz[q], gx2[q], gy2[q], gz2[q], false, false);
+          else interact2<POT, DN, false, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], false,
+                                                false, a.flag);
+        }
       }
       int k1 = mlo + ((sub - mlo) % S + S) % S;
       for (int k = k1; k < mhi; k += step) {
         const int o = own[k];
         const float4 sv = tile[k];
 #pragma unroll
-        for (int q = 0; q < NP; ++q)
-          interact2<POT, DN, true, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q], o == ti[2 * q],
-                                          o == ti[2 * q + 1], a.flag);
+        for (int q = 0; q < NP; ++q) {
+          if (SC) interact2s<true>(sv, px[q], py[q], pz[q], gx2[q], gy2[q], gz2[q], o == ti[2 * q], o == ti[2 * q + 1]);
+          else interact2<POT, DN, true, CHECK>(sv, px[q], py[q], pz[q], ap2[q], gx2[q], gy2[q], gz2[q],
+                                               o == ti[2 * q], o == ti[2 * q + 1], a.flag);
+        }
       }
     }
   }
@@ -285,9 +322,10 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
 constexpr int P2P_T = 4;
 
 template <bool SELF, bool CHECK>
-void dispatch(const P2PArgs& a, bool pot, bool dn, int grid, cudaStream_t st) {
+void dispatch(const P2PArgs& a, bool pot, bool dn, bool scaled, int grid, cudaStream_t st) {
   if (pot && dn) k_p2p<P2P_T, true, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
   else if (pot) k_p2p<P2P_T, true, false, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+  else if (scaled && !CHECK) k_p2p<P2P_T, false, true, SELF, false, true><<<grid, 32, 0, st>>>(a);
   else k_p2p<P2P_T, false, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
 }
 
@@ -385,12 +423,13 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   a.flag = c->flag.get();
   if (dn && !a.tnrm) throw Error(FMMBEM_E_INVALID, "normal derivative requested at targets without normals");
   const int grid = (int)items.n;
+  const bool sc = c->p2p_scaled != 0;
   if (self) {
-    if (check) dispatch<true, true>(a, pot, dn, grid, st);
-    else dispatch<true, false>(a, pot, dn, grid, st);
+    if (check) dispatch<true, true>(a, pot, dn, sc, grid, st);
+    else dispatch<true, false>(a, pot, dn, sc, grid, st);
   } else {
-    if (check) dispatch<false, true>(a, pot, dn, grid, st);
-    else dispatch<false, false>(a, pot, dn, grid, st);
+    if (check) dispatch<false, true>(a, pot, dn, sc, grid, st);
+    else dispatch<false, false>(a, pot, dn, sc, grid, st);
   }
   FMM_CHECK_LAUNCH();
 }
