@@ -738,10 +738,12 @@ void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st) {
 
 template <int P, int W>
 void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devices = 0;  // the attribute is per device: set it once on each
+  int dev = 0;
+  FMM_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !(attr_devices >> dev & 1ULL)) {
     FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    attr_devices |= 1ULL << dev;
   }
   k_m2l_rot_sync<P, W><<<ceil_div(w.rows, W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
                                                                    w.idx.get(), T.key.get(), c->Mx.get(),

@@ -1,2 +1,5 @@
-python -m pytest tests -m gpu -q 2>&1 | tail -2
-python bench.py --steps 10 --warmup 3 > gpurun_out/bench_sc.json 2>/dev/null; python -c "import json; d=json.load(open('gpurun_out/bench_sc.json')); print(d['ms_per_step'], d['phases_ms'], d['parity_sampled_rows'], d['e2e'], d['roofline'])"
+python -m pytest tests/test_gpu_parity.py -q -x -k "fmm or rot" 2>&1 | tail -1
+for v in 1 4 8 1; do
+  echo "== ml $v"; FMMBEM_ML_WARPS=$v python bench.py --steps 5 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(round(d['ms_per_step'],2), {k:round(v,2) for k,v in d['phases_ms'].items()})"
+done
+FMMBEM_ML_WARPS=8 python -m pytest tests/test_gpu_parity.py -q -x -k "fmm or rot" 2>&1 | tail -1
