@@ -746,12 +746,17 @@ fmmbem_status fmmbem_matvec(fmmbem_ctx* c, fmmbem_op op, const float* x, float* 
 }
 
 // Host-buffer matvec with the transfers pipelined against the kernels (single GPU, K = 1, no
-// near-field option): x arrives in NCH Morton-contiguous chunks on a copy stream and P2M of each
+// near-field option): x arrives in NCH (default 8) Morton-contiguous chunks on a copy stream and P2M of each
 // chunk's leaves starts as soon as it lands; the far field runs next and L2P writes y first; P2P
 // then adds the near field chunk by chunk and each chunk of y leaves for the host while the next
 // chunk computes.  Same operations as apply_op (P2P and L2P swap order; P2P accumulates).
 void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* yh) {
-  constexpr int NCH = 4;
+  constexpr int NCH_MAX = 16;
+  static const int NCH = [] {  // transfer chunks (FMMBEM_E2E_CHUNKS, default 8)
+    const char* e = std::getenv("FMMBEM_E2E_CHUNKS");
+    const int v = e ? std::atoi(e) : 8;
+    return v < 1 ? 1 : (v > 16 ? 16 : v);
+  }();
   cudaStream_t st = c->stream;
   const Tree& T = c->tree;
   const int64_t np = c->np;
@@ -764,7 +769,7 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
     FMM_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
     for (auto& e : c->pev) FMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  int lb[NCH + 1];
+  int lb[NCH_MAX + 1];
   lb[0] = 0;
   for (int k = 1; k < NCH; ++k) {
     const int64_t goal = np * k / NCH;
@@ -775,8 +780,8 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
   float* x = c->tmp_x.get();
   float* y = c->tmp_y.get();
   cudaEvent_t* eh = c->pev;            // x chunk k on the device
-  cudaEvent_t* ep = c->pev + NCH;      // y chunk k final
-  cudaEvent_t e0 = c->pev[2 * NCH];    // previous work on st done with tmp_x / tmp_y
+  cudaEvent_t* ep = c->pev + NCH_MAX;  // y chunk k final
+  cudaEvent_t e0 = c->pev[2 * NCH_MAX];  // previous work on st done with tmp_x / tmp_y
   FMM_CUDA(cudaEventRecord(e0, st));
   FMM_CUDA(cudaStreamWaitEvent(c->cstream, e0, 0));
   for (int k = 0; k < NCH; ++k) {

@@ -101,7 +101,7 @@ struct fmmbem_ctx {
   fmm::DevBuf<float> tmp_x, tmp_y;  // host-buffer matvec staging / scratch
   std::vector<int> h_pan_begin;      // host copy of pan.begin (pipelined host-buffer matvec)
   cudaStream_t cstream = nullptr;    // copy stream of the pipelined host-buffer matvec
-  cudaEvent_t pev[9] = {};           // its chunk events (2 x 4 + 1)
+  cudaEvent_t pev[33] = {};          // its chunk events (2 x 16 + 1)
   fmm::DevBuf<float> En, psi;       // charge fields (cached)
   bool have_fields = false;
   fmm::DevBuf<int> flag;            // device error flags
