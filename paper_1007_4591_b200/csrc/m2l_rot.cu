@@ -241,35 +241,44 @@ __device__ __forceinline__ void translate_pair(const Slot& sl, int tx, int ty, i
 // Lockstep variant: the W warps of a CTA (one target row each) start every 32-pair round together
 // (__syncthreads per round), so the SM's warps walk the long unrolled body in step and share the
 // instruction-cache lines (the body is ~3x the L1.5 I$); dynamic shared memory, W slots.
-template <int P, int W>
+template <int P, int W, int RPW>
 __global__ void __launch_bounds__(32 * W) k_m2l_rot_sync(int rows, const int* __restrict__ tcells,
                                                          const int* __restrict__ off, const int* __restrict__ idx,
                                                          const uint64_t* __restrict__ key,
                                                          const float2* __restrict__ M, float2* __restrict__ Lx) {
+  // A CTA owns RPW x W consecutive rows (Morton-local); a warp that finishes its row takes the next
+  // unclaimed one of the window at the next round, so rows of different lengths do not leave warps
+  // idle at the round barriers.  Each row is computed whole by the warp that claims it (fixed chunk
+  // order), so the result does not depend on which warp that is.
   constexpr int NC = P * (P + 1) / 2;
   constexpr int NR = (NC + 31) / 32;
   extern __shared__ float2 svdyn[];
-  __shared__ int rounds_w[W];
+  __shared__ int next_row;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * W + w;
-  const bool has = row < rows;
+  const int r_beg = blockIdx.x * W * RPW, r_end = min(rows, r_beg + W * RPW);
+  if (threadIdx.x == 0) next_row = r_beg + W;
   float2* sv = svdyn + (size_t)w * NC * 33;
-  const int cell = has ? tcells[row] : 0;
-  const int lo = has ? off[row] : 0, hi = has ? off[row + 1] : 0;
-  if (lane == 0) rounds_w[w] = (hi - lo + 31) / 32;
-  __syncthreads();
-  int rounds = 0;
-#pragma unroll
-  for (int k = 0; k < W; ++k) rounds = max(rounds, rounds_w[k]);
   const Slot sl{sv + lane};
-  int tx = 0, ty = 0, tz = 0;
-  if (has) demorton(key[cell], tx, ty, tz);
+  int row = r_beg + w;
+  int cell = 0, lo = 0, hi = 0, e0 = 0, tx = 0, ty = 0, tz = 0;
+  auto start = [&]() {
+    if (row < r_end) {
+      cell = tcells[row];
+      lo = off[row];
+      hi = off[row + 1];
+      e0 = lo;
+      demorton(key[cell], tx, ty, tz);
+    }
+  };
+  start();
   float2 acc[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r] = make_float2(0.f, 0.f);
-  for (int rd = 0; rd < rounds; ++rd) {
-    const int e0 = lo + 32 * rd;
-    if (e0 < hi) {
+  __syncthreads();
+  while (true) {
+    const bool active = row < r_end;
+    if (!__syncthreads_or(active)) break;  // the round barrier; ends when every warp is out of rows
+    if (active) {
       const int e = e0 + lane;
       if (e < hi) {
         translate_pair<P>(sl, tx, ty, tz, idx[e], key, M);
@@ -288,18 +297,25 @@ __global__ void __launch_bounds__(32 * W) k_m2l_rot_sync(int rows, const int* __
           acc[r] = __fadd2_rn(acc[r], sum);
         }
       }
-    }
-    __syncthreads();
-  }
-  if (!has) return;
+      __syncwarp();
+      e0 += 32;
+      if (e0 >= hi) {  // row done: flush, claim the next row of the window
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const int c = lane + 32 * r;
-    if (c < NC) {
-      float2 o = Lx[(size_t)cell * NC + c];
-      o.x += acc[r].x;
-      o.y += acc[r].y;
-      Lx[(size_t)cell * NC + c] = o;
+        for (int r = 0; r < NR; ++r) {
+          const int c = lane + 32 * r;
+          if (c < NC) {
+            float2 o = Lx[(size_t)cell * NC + c];
+            o.x += acc[r].x;
+            o.y += acc[r].y;
+            Lx[(size_t)cell * NC + c] = o;
+          }
+          acc[r] = make_float2(0.f, 0.f);
+        }
+        int nr = 0;
+        if (lane == 0) nr = atomicAdd(&next_row, 1);
+        row = __shfl_sync(0xffffffffu, nr, 0);
+        start();
+      }
     }
   }
 }
@@ -742,10 +758,10 @@ void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem
   int dev = 0;
   FMM_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !(attr_devices >> dev & 1ULL)) {
-    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_devices |= 1ULL << dev;
   }
-  k_m2l_rot_sync<P, W><<<ceil_div(w.rows, W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
+  k_m2l_rot_sync<P, W, 16><<<ceil_div(w.rows, 16 * W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
                                                                    w.idx.get(), T.key.get(), c->Mx.get(),
                                                                    c->Lx.get());
 }
