@@ -122,13 +122,17 @@ typedef enum {
 /* One FMM matrix-vector product.  x_dev, y_dev: caller-owned device
  * arrays of fmmbem_num_local_panels floats in local order; must not alias.  Stream-ordered:
  * returns after enqueueing on cuda_stream; y is valid when the stream completes.  With nranks > 1
- * the call is collective (all ranks, same order): x slices are all-gathered and the partial
- * multipoles of every rank's subtrees are all-reduced over NCCL. */
+ * the call is collective (all ranks, same order): x slices are all-gathered and the multipoles
+ * each rank's interaction lists need are exchanged over NCCL (local essential tree). */
 fmmbem_status fmmbem_matvec(fmmbem_ctx* ctx, fmmbem_op op, const float* x_dev, float* y_dev,
                             void* cuda_stream);
 
-/* Same product with HOST buffers (pinned or pageable): copies x in, runs, copies y out,
- * synchronises.  Used for end-to-end timing. */
+/* Same product with HOST buffers (pinned or pageable; pinned lets the transfers overlap):
+ * x_host / y_host hold the rank's n_local values in local order.  Single GPU: x is copied in
+ * Morton-contiguous chunks on an internal copy stream while P2M starts on the chunks that have
+ * landed, and y leaves in chunks as P2P finishes them (same result as fmmbem_matvec up to the
+ * rounding of the near + far addition).  nranks > 1: copy in, fmmbem_matvec, copy out.  Blocks
+ * until y_host is written.  Errors as fmmbem_matvec. */
 fmmbem_status fmmbem_matvec_host(fmmbem_ctx* ctx, fmmbem_op op, const float* x_host, float* y_host);
 
 typedef struct {
