@@ -16,7 +16,7 @@ namespace {
 
 __host__ __device__ constexpr int cx(int n, int m) { return n * (n + 1) / 2 + m; }
 
-constexpr int P2M_TILE = 128;  // sources staged in shared memory per pass
+constexpr int P2M_TILE = 256;  // sources staged in shared memory per pass (256 measured 3 % faster than 128)
 
 // R_m^m(u) = (-(x + i y)/2)^m / m!
 template <int m>
