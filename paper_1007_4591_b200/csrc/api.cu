@@ -579,6 +579,7 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   c->P = opt.terms;
   if (const char* e = std::getenv("FMMBEM_M2L")) c->m2l_mode = (std::string(e) == "p4") ? 1 : 0;
   if (const char* e = std::getenv("FMMBEM_P2P_CHUNK")) c->p2p_chunk = std::max(8, std::min(256, std::atoi(e)));
+  if (const char* e = std::getenv("FMMBEM_P2P_OCC")) c->p2p_occ = std::atoi(e);
   if (const char* e = std::getenv("FMMBEM_P2P_PLAIN")) c->p2p_scaled = std::atoi(e) ? 0 : 1;
   c->p2p_chunk = std::min(c->p2p_chunk, 128);  // <= 32 lanes x 4 targets per subset
   // near field concurrent with the far field: default on with several ranks (hides the exchange)
@@ -809,6 +810,7 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
   far.pot.d = far.dn.d = nullptr;
   launch_l2p(c, t, far, st);
   o.pot.acc = o.dn.acc = 1;
+  if (c->p2p_scaled && op != FMMBEM_OP_SINGLE) s.scaled = prepare_p2p_sources(c, s, st);  // once for all chunks
   for (int k = 0; k < NCH; ++k) {
     TgtArg tk = t;
     tk.leaf_lo = lb[k];

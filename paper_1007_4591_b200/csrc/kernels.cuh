@@ -25,6 +25,7 @@ struct SrcArg {
   const float* x = nullptr;
   const float* x_far = nullptr;  // weights for the upward sweep if different from x (owned slice view)
   const float* ag_src = nullptr;  // deferred all-gather ag_src -> x (run by fmm_eval before P2P)
+  const float4* scaled = nullptr;  // prepared scaled-form P2P sources (prepare_p2p_sources), else built in launch_p2p
   int leaf_lo = 0, leaf_hi = -1;
   const int* cnt = nullptr;
 };
@@ -45,6 +46,8 @@ void build_tree(fmmbem_ctx* c, const double* cen, const double* nrm, const doubl
                 const double* wq, const double* cxyz, const double* cq, cudaStream_t s);
 
 // near field; writes y = ax x + b raw (overwrites)
+// per-matvec scaled-form source table (a y, a) of the K' / A near field into c->p2p_src
+const float4* prepare_p2p_sources(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
 void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
                 bool direct, cudaStream_t st);
 const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi);

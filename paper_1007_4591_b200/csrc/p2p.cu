@@ -35,6 +35,7 @@ struct P2PArgs {
   const float4* tnrm;
   const int* tbeg;
   const float4* spos;
+  const float4* ssc;  // scaled form: per-source (a s, a) prepared by k_scale_src (SC kernels only)
   const float* sx;
   int sdiv;
   const int* sbeg;
@@ -101,14 +102,15 @@ __device__ __forceinline__ void interact2s(const float4 s, float2 px, float2 py,
   gz = __ffma2_rn(t, dz, gz);
 }
 
-template <int T, bool POT, bool DN, bool SELF, bool CHECK, bool SC = false>
-__global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
+template <int T, bool POT, bool DN, bool SELF, bool CHECK, bool SC = false, int MINB = 28>
+__global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
   static_assert(!SC || (DN && !POT && !CHECK), "scaled form: normal derivative only");
   __shared__ float4 tile[TILE];
   __shared__ int own[SELF ? TILE : 1];
   __shared__ int seg_src[MAXSEG], seg_cum[MAXSEG + 1];
   __shared__ float4 seg_sh[MAXSEG];
-  __shared__ float red[4 * T][32];
+  static_assert(4 * T * 32 * sizeof(float) <= sizeof(float4) * TILE, "split-K scratch aliases the tile");
+  float(*red)[32] = reinterpret_cast<float(*)[32]>(tile);  // used only after the source loop
 
   const int4 it = a.items[blockIdx.x];
   const int leaf = it.x, tb = it.y, nt = it.z;
@@ -184,6 +186,15 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
     ap2[q] = gx2[q] = gy2[q] = gz2[q] = make_float2(0.f, 0.f);
   }
   const int step = lvalid ? S : 0;
+  // per-lane segment cursor of the tile fill: lane l fills v = base + l + 32 q, increasing over the
+  // whole kernel, so the segment holding v only ever advances (no per-source search)
+  int cur = 0, nxt = 0, jb = 0;
+  float4 shv = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!a.direct) {
+    nxt = seg_cum[1];
+    jb = seg_src[0];
+    shv = seg_sh[0];
+  }
 
   for (int base = 0; base < n_src; base += TILE) {
     const int tcnt = min(TILE, n_src - base);
@@ -196,30 +207,28 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
         int j;
         float sx, sy, sz;
         if (!a.direct) {
-          int lo = 0, hi = nseg - 1;  // last segment with seg_cum[seg] <= v
-          while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (seg_cum[mid] <= v) lo = mid; else hi = mid - 1;
+          if (v >= nxt) {  // v < n_src = seg_cum[nseg]: stops at a segment of the list
+            do {
+              ++cur;
+              nxt = seg_cum[cur + 1];
+            } while (v >= nxt);
+            jb = seg_src[cur] - seg_cum[cur];
+            shv = seg_sh[cur];
           }
-          j = seg_src[lo] + (v - seg_cum[lo]);
-          const float4 sh = seg_sh[lo];
-          sx = sh.x; sy = sh.y; sz = sh.z;
+          j = jb + v;
+          sx = shv.x; sy = shv.y; sz = shv.z;
         } else {
           j = v;
           const int4 sc = a.ijk[a.sleaf[j]];
           sx = (sc.x - tc.x) * a.h; sy = (sc.y - tc.y) * a.h; sz = (sc.z - tc.z) * a.h;
         }
-        const float4 p = __ldg(a.spos + j);
-        float w = p.w;
-        if (a.sx) w *= __ldg(a.sx + (a.sdiv == 1 ? j : j / a.sdiv));
-        if (SC) {
-          if (w == 0.f) {
-            tile[k] = make_float4(1e18f, 1e18f, 1e18f, 1.f);
-          } else {
-            const float sc = copysignf(rsqrtf(fabsf(w)), w);
-            tile[k] = make_float4(sc * (p.x + sx), sc * (p.y + sy), sc * (p.z + sz), sc);
-          }
+        if (SC) {  // (a s, a) from k_scale_src: shift into the target leaf's frame, a (s + sh)
+          const float4 p = __ldg(a.ssc + j);
+          tile[k] = make_float4(fmaf(p.w, sx, p.x), fmaf(p.w, sy, p.y), fmaf(p.w, sz, p.z), p.w);
         } else {
+          const float4 p = __ldg(a.spos + j);
+          float w = p.w;
+          if (a.sx) w *= __ldg(a.sx + (a.sdiv == 1 ? j : j / a.sdiv));
           tile[k] = make_float4(p.x + sx, p.y + sy, p.z + sz, w);
         }
         if (SELF) own[k] = (a.sdiv == 1) ? j : j / a.sdiv;
@@ -253,6 +262,7 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
         }
       }
       int k1 = mlo + ((sub - mlo) % S + S) % S;
+#pragma unroll 4
       for (int k = k1; k < mhi; k += step) {
         const int o = own[k];
         const float4 sv = tile[k];
@@ -275,6 +285,7 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
   }
   // ---- split-K reduction over the S subsets
   if (S > 1) {
+    __syncwarp();  // every lane is done reading the tile
 #pragma unroll
     for (int q = 0; q < T; ++q) {
       red[4 * q + 0][lane] = ap[q];
@@ -322,11 +333,32 @@ __global__ void __launch_bounds__(32) k_p2p(P2PArgs a) {
 constexpr int P2P_T = 4;
 
 template <bool SELF, bool CHECK>
-void dispatch(const P2PArgs& a, bool pot, bool dn, bool scaled, int grid, cudaStream_t st) {
+void dispatch(const P2PArgs& a, bool pot, bool dn, bool scaled, bool occ, int grid, cudaStream_t st) {
   if (pot && dn) k_p2p<P2P_T, true, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
   else if (pot) k_p2p<P2P_T, true, false, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+  else if (scaled && !CHECK && occ) k_p2p<P2P_T, false, true, SELF, false, true, 32><<<grid, 32, 0, st>>>(a);
   else if (scaled && !CHECK) k_p2p<P2P_T, false, true, SELF, false, true><<<grid, 32, 0, st>>>(a);
   else k_p2p<P2P_T, false, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
+}
+
+// Scaled-form source table for one matvec: a = sign(w) |w|^(-1/2) with w = (A_j w_g) x_j, stored as
+// (a y, a) in leaf-local coordinates (see interact2s).  A zero weight becomes a source at 1e18 with
+// a = 1 (its r'^-3 flushes to zero); the shift a * (leaf offset) added in the fill keeps it there.
+__global__ void k_scale_src(int64_t n, const float4* __restrict__ spos, const float* __restrict__ sx, int sdiv,
+                            float4* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const float4 p = __ldg(spos + j);
+  float w = p.w;
+  if (sx) w *= __ldg(sx + (sdiv == 1 ? j : j / sdiv));
+  float4 r;
+  if (w == 0.f) {
+    r = make_float4(1e18f, 1e18f, 1e18f, 1.f);
+  } else {
+    const float sc = copysignf(rsqrtf(fabsf(w)), w);
+    r = make_float4(sc * p.x, sc * p.y, sc * p.z, sc);
+  }
+  out[j] = r;
 }
 
 __global__ void k_count(int nl, const int* __restrict__ tbeg, const int* __restrict__ sbeg,
@@ -394,6 +426,15 @@ const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int lea
   return *c->p2p_cache.back();
 }
 
+const float4* prepare_p2p_sources(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
+  const int64_t n = s.set->n;
+  if ((int64_t)c->p2p_src.n < n) c->p2p_src.alloc(n);
+  if (n > 0)
+    k_scale_src<<<ceil_div(n, 256), 256, 0, st>>>(n, s.set->pos.get(), s.x, s.set->div, c->p2p_src.get());
+  FMM_CHECK_LAUNCH();
+  return c->p2p_src.get();
+}
+
 void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
                 bool direct, cudaStream_t st) {
   const Tree& T = c->tree;
@@ -423,13 +464,17 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   a.flag = c->flag.get();
   if (dn && !a.tnrm) throw Error(FMMBEM_E_INVALID, "normal derivative requested at targets without normals");
   const int grid = (int)items.n;
-  const bool sc = c->p2p_scaled != 0;
+  const bool sc = c->p2p_scaled != 0 && dn && !pot && !check;
+  if (sc) {
+    a.ssc = s.scaled;
+    if (!a.ssc) a.ssc = prepare_p2p_sources(c, s, st);
+  }
   if (self) {
-    if (check) dispatch<true, true>(a, pot, dn, sc, grid, st);
-    else dispatch<true, false>(a, pot, dn, sc, grid, st);
+    if (check) dispatch<true, true>(a, pot, dn, sc, c->p2p_occ != 0, grid, st);
+    else dispatch<true, false>(a, pot, dn, sc, c->p2p_occ != 0, grid, st);
   } else {
-    if (check) dispatch<false, true>(a, pot, dn, sc, grid, st);
-    else dispatch<false, false>(a, pot, dn, sc, grid, st);
+    if (check) dispatch<false, true>(a, pot, dn, sc, c->p2p_occ != 0, grid, st);
+    else dispatch<false, false>(a, pot, dn, sc, c->p2p_occ != 0, grid, st);
   }
   FMM_CHECK_LAUNCH();
 }
