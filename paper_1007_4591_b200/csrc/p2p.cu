@@ -12,7 +12,7 @@
 // target leaf's frame: offsets between leaf centres are exact multiples of the leaf width
 // (FP32-exact), so s - x subtracts two numbers of leaf size only.  All lanes of a
 // subset read the same source (broadcast LDS.128).  Outputs are owned by one lane (no atomics,
-// fixed summation order -> bitwise reproducible).  Only the self-leaf block is masked (j != i of
+// fixed summation order -> bitwise reproducible).  Only the chunk's own sources are masked (j != i of
 // the discrete operator).
 //
 // Raw outputs, un-normalised potential phi = sum_j w_j / r_ij:
@@ -150,16 +150,16 @@ __global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
     __syncwarp();
     nseg = nn;
     n_src = seg_cum[nn];
-    if (SELF) {
-      self_lo = seg_cum[nn - 1];
-      self_hi = n_src;
+    if (SELF) {  // only the chunk's own sources j / sdiv in [tb, tb + nt) need the j != i mask
+      self_lo = seg_cum[nn - 1] + (tb * a.sdiv - seg_src[nn - 1]);
+      self_hi = self_lo + nt * a.sdiv;
     } else {
       self_lo = self_hi = n_src;
     }
   } else {
     n_src = a.ns;
-    self_lo = a.sbeg[leaf];
-    self_hi = a.sbeg[leaf + 1];
+    self_lo = tb * a.sdiv;
+    self_hi = (tb + nt) * a.sdiv;
   }
 
   // ---- lane mapping: tl-th target slot, source subset sub of S
