@@ -26,7 +26,15 @@ namespace fmm {
 
 namespace {
 
-constexpr int TILE = 256;   // sources per warp tile (256 with unroll 16 measured fastest: 128 / 512 tiles, unroll 4 / 8 / 32 slower)
+#ifndef P2P_TILE
+#define P2P_TILE 256
+#endif
+#ifndef P2P_UNROLL
+#define P2P_UNROLL 16
+#endif
+#define P2P_PRAGMA(x) _Pragma(#x)
+#define P2P_UNROLL_LOOP(n) P2P_PRAGMA(unroll n)
+constexpr int TILE = P2P_TILE;   // sources per warp tile (256 with unroll 16 measured fastest: 128 / 512 tiles, unroll 4 / 8 / 32 slower)
 constexpr int MAXSEG = 32;
 
 struct P2PArgs {
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
     const int mlo = SELF ? min(max(self_lo - base, 0), tcnt) : tcnt;
     const int mhi = SELF ? min(max(self_hi - base, 0), tcnt) : tcnt;
     // unmasked: [0, mlo) and [mhi, tcnt)
-#pragma unroll 16
+P2P_UNROLL_LOOP(P2P_UNROLL)
     for (int k = sub; k < mlo; k += step) {
       const float4 sv = tile[k];
 #pragma unroll
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
     }
     if (SELF) {
       int k0 = mhi + ((sub - mhi) % S + S) % S;
-#pragma unroll 16
+P2P_UNROLL_LOOP(P2P_UNROLL)
       for (int k = k0; k < tcnt; k += step) {
         const float4 sv = tile[k];
 #pragma unroll
