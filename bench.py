@@ -46,11 +46,12 @@ def m2l_rot_flops(P):
 
 def launches_per_matvec(L, P):
     """libfmmbem kernels per A-matvec: P2M, M2M per level (rotation: translate + sum), one M2L,
-    L2L per level, P2P, L2P (memsets and NCCL kernels excluded)."""
+    L2L per level, the scaled P2P source table (k_scale_src), P2P, L2P (memsets and NCCL kernels
+    excluded)."""
     if L < 2:
-        return 1
+        return 2
     m2m = 2 if P in (8, 10, 12) else 1
-    return 1 + m2m * (L - 2) + 1 + (L - 2) + 1 + 1
+    return 1 + m2m * (L - 2) + 1 + (L - 2) + 1 + 1 + 1
 
 
 def workload(name):

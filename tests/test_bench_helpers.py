@@ -25,9 +25,9 @@ def test_m2l_flops_per_translation():
 
 def test_launches_per_matvec_c5():
     b = _bench()
-    # leaf level 8: P2M, 6 x (M2M rotate + sum), M2L, 6 L2L, P2P, L2P
-    assert b.launches_per_matvec(8, 12) == 1 + 2 * 6 + 1 + 6 + 1 + 1 == 22
-    assert b.launches_per_matvec(1, 12) == 1  # no far field: P2P only
+    # leaf level 8: P2M, 6 x (M2M rotate + sum), M2L, 6 L2L, P2P source table, P2P, L2P
+    assert b.launches_per_matvec(8, 12) == 1 + 2 * 6 + 1 + 6 + 1 + 1 + 1 == 23
+    assert b.launches_per_matvec(1, 12) == 2  # no far field: source table + P2P
 
 
 def test_p2p_flop_convention():
