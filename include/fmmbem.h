@@ -18,6 +18,12 @@
  * Errors: every call returns fmmbem_status; nothing throws across the ABI; on a
  * negative status no output has been written ("no partial outputs") and
  * fmmbem_last_error() names the offending index.  A ctx is not thread-safe.
+ * Ordering: fmmbem_matvec is stream-ordered on the caller's stream; every other call that touches
+ * the device is BLOCKING (it returns when its results are written) and runs on the ctx's internal
+ * stream.  Every call -- matvec included -- first waits (on the device) for the work of the previous
+ * call on this ctx, whatever stream that ran on, because all calls share the ctx's expansion and
+ * staging buffers.  Device buffers passed to a blocking call must not be in use by pending work on
+ * other streams (the Python binding synchronises the caller's current stream before such calls).
  * Units: Angstrom and elementary charges; energies in internal units (kernels with the
  * explicit 1/(4 pi) of Eq. 4-5) and in kcal/mol = internal * 4 pi * 332.0637.
  */
@@ -30,7 +36,7 @@
 extern "C" {
 #endif
 
-#define FMMBEM_ABI_VERSION 1
+#define FMMBEM_ABI_VERSION 2
 
 typedef struct fmmbem_ctx fmmbem_ctx; /* opaque */
 
@@ -76,9 +82,19 @@ typedef struct {
   int32_t direct;        /* 1 = bypass the FMM: all-pairs P2P (paper Fig. 11 "direct") */
   int32_t deterministic; /* reductions have a fixed order (no atomics on results); always true */
   int32_t device;        /* CUDA ordinal used by this ctx */
-  int32_t rank, nranks;  /* one process per GPU; every rank passes the FULL mesh and charges */
+  int32_t rank, nranks;  /* one process per GPU, nranks <= 64; every rank passes ALL charges */
   const void* nccl_id;   /* nranks > 1: the 128-byte id from fmmbem_get_unique_id() on rank 0, broadcast by the caller */
+  int32_t input_mode;    /* nranks > 1 only.  0: every rank passes the FULL mesh (rank r prepares triangles
+                            [r n/R, (r+1) n/R), global id = triangle index).  1: every rank passes only ITS
+                            part of the mesh (its own vertex array; triangles index it); the global id of rank
+                            r's triangle k is k + (triangles of ranks < r) -- memory O(N/R) per rank (SURVEY
+                            8(e)); near_mode and self_term need mode 0.  Either way the panels move to the rank
+                            owning their leaf; default 0 */
 } fmmbem_options;
+
+/* FMMBEM_ABI_VERSION of the built library; sizes of the ABI structs (bindings check these). */
+int32_t fmmbem_abi_version(void);
+int64_t fmmbem_struct_size(const char* name); /* "options", "timing", "energy", "tree_info", "solve_options"; -1 if unknown */
 
 /* Fill *out with the defaults above.  Returns FMMBEM_E_INVALID if out is NULL. */
 fmmbem_status fmmbem_default_options(fmmbem_options* out);
@@ -109,7 +125,8 @@ void fmmbem_destroy(fmmbem_ctx* ctx);
 /* Vectors passed to matvec/solve/bibee are in the library's LOCAL order (the octree's
  * Morton order) and, with nranks > 1, hold only this rank's panels (a contiguous range of
  * Morton-ordered leaves of equal estimated work).  fmmbem_local_panel_ids writes, for local
- * index i, the caller's triangle index (host int64 array of fmmbem_num_local_panels entries). */
+ * index i, the panel's GLOBAL id (host int64 array of fmmbem_num_local_panels entries): the caller's
+ * triangle index (one rank, input_mode 0) or the id defined by input_mode 1. */
 int64_t fmmbem_num_local_panels(const fmmbem_ctx* ctx);
 fmmbem_status fmmbem_local_panel_ids(const fmmbem_ctx* ctx, int64_t* global_ids_out);
 
@@ -167,6 +184,10 @@ typedef enum {
 fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* ctx, fmmbem_bibee variant, float* sigma_hat_dev,
                                   fmmbem_energy* out);
 
+/* Drop the cached E_n / psi of the charge-FMM, so that the next bibee / solve / charge_fields call
+ * recomputes them (benchmarks of the uncached BIBEE energy).  Host only; never fails on a valid ctx. */
+fmmbem_status fmmbem_reset_fields(fmmbem_ctx* ctx);
+
 /* Diagnostics: E_n (with 1/eps_I) and psi_j = sum_g w_g sum_k q_k G(y_jg, r_k) at the panels
  * (device, local order; either may be NULL). */
 fmmbem_status fmmbem_charge_fields(fmmbem_ctx* ctx, float* En_dev, float* psi_dev);
@@ -176,10 +197,14 @@ fmmbem_status fmmbem_charge_fields(fmmbem_ctx* ctx, float* En_dev, float* psi_de
 fmmbem_status fmmbem_reaction_potential(fmmbem_ctx* ctx, const float* sigma_dev, double* phi_host);
 
 typedef struct {
-  double tree, upward, m2l, p2p, l2p, near, comm, gmres, total; /* ms of the last matvec:
-                             upward = P2M + M2M, m2l = M2L, l2p = L2L + L2P, comm = NCCL exchanges, gmres = last solve */
+  double tree, upward, m2l, p2p, l2p, near, comm, gmres, total; /* ms: tree = octree build at
+                             create (keys, sort, levels, lists, point placement; host clock); the rest = the last
+                             matvec (CUDA events on the stream each phase ran on): upward = P2M + M2M, m2l = M2L,
+                             l2p = L2L + L2P, comm = NCCL exchanges, total = the whole product; gmres = last solve */
   int64_t p2p_interactions; /* exact pair count of the last matvec's P2P */
   int64_t m2l_pairs;        /* M2L translations of the last matvec */
+  double p2m, m2m, l2l, leaf_l2p; /* ms, the last matvec: upward = p2m + m2m, l2p = l2l + leaf_l2p */
+  double bibee;             /* ms of the last fmmbem_bibee_energy (charge-FMM if not cached + reduction; CUDA events) */
 } fmmbem_timing;
 
 fmmbem_status fmmbem_last_timing(const fmmbem_ctx* ctx, fmmbem_timing* out);
@@ -197,6 +222,32 @@ typedef struct {
 } fmmbem_tree_info;
 
 fmmbem_status fmmbem_tree_info_get(const fmmbem_ctx* ctx, fmmbem_tree_info* out);
+
+/* The multi-GPU exchange plan of a leaf skeleton, computed on the HOST by the same
+ * code fmmbem_create runs on every rank: the cost-weighted contiguous leaf partition, the
+ * near-field halo (leaves whose panels a peer's P2P needs) and the local essential tree (pure cells
+ * whose multipoles a peer's M2L needs; cells straddling ranks, summed by all-reduce).  For
+ * tests and tooling; no GPU is used.  leaf_keys: n_leaves sorted unique Morton keys at `level`
+ * (x least significant); leaf_panels / leaf_charges (nullable): points per leaf of ALL ranks;
+ * quad_points = K.  Lists are read with fmmbem_plan_list: returns the count and, if out is non-NULL,
+ * writes the entries (int64).  Leaves are leaf indices; cells are level-major global cell indices
+ * (FMMBEM_PLAN_CELL_KEYS / _LEVEL_OFFSETS give the cell numbering). */
+typedef struct fmmbem_plan fmmbem_plan;
+enum {
+  FMMBEM_PLAN_HALO_SEND = 0,   /* peer: my leaves whose panels peer needs */
+  FMMBEM_PLAN_HALO_RECV = 1,   /* peer: peer's leaves whose panels I need */
+  FMMBEM_PLAN_LET_SEND = 2,    /* peer: my pure cells whose multipoles peer needs */
+  FMMBEM_PLAN_LET_RECV = 3,    /* peer: peer's pure cells I need */
+  FMMBEM_PLAN_LET_SHARED = 4,  /* cells straddling ranks (peer ignored) */
+  FMMBEM_PLAN_LEAF_BOUNDS = 5, /* nranks + 1 leaf bounds */
+  FMMBEM_PLAN_CELL_KEYS = 6,   /* every cell's key, level-major */
+  FMMBEM_PLAN_LEVEL_OFFSETS = 7 /* level + 2 offsets into the cell numbering */
+};
+fmmbem_status fmmbem_plan_create(const uint64_t* leaf_keys, const int32_t* leaf_panels, const int32_t* leaf_charges,
+                                 int64_t n_leaves, int32_t level, int32_t quad_points, int32_t nranks, int32_t rank,
+                                 fmmbem_plan** out);
+void fmmbem_plan_destroy(fmmbem_plan* plan);  /* NULL-safe */
+int64_t fmmbem_plan_list(const fmmbem_plan* plan, int32_t list, int32_t peer, int64_t* out); /* -1: bad list / peer */
 
 /* Thread-local message describing the last error (never NULL). */
 const char* fmmbem_last_error(void);

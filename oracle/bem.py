@@ -99,11 +99,21 @@ def constants(eps_in: float, eps_out: float):
     return 2.0 * (eps_out - eps_in) / (eps_in + eps_out), 1.0 - eps_in / eps_out
 
 
-def normal_field(pan: Panels, cxyz, cq, eps_in: float):
+def normal_field(pan: Panels, cxyz, cq, eps_in: float, rows=None):
     """O3: E_i = (1/eps_I) sum_k q_k dG/dn_i(c_i, r_k)  (Eq. 1's 1/eps_I; Eq. 4; A2)."""
+    idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)
     if len(cq) == 0:
-        return np.zeros(pan.n)
-    return _cdirect.dn_sum(pan.centroid, pan.normal, None, cxyz, cq, None) / eps_in
+        return np.zeros(len(idx))
+    return _cdirect.dn_sum(pan.centroid[idx], pan.normal[idx], None, cxyz, cq, None) / eps_in
+
+
+def charge_potential(pan: Panels, cxyz, cq, rows=None):
+    """psi_i = sum_k q_k G(c_i, r_k) at the centroids (K = 1): the charges' Coulomb potential whose
+    area-weighted sum with sigma gives Delta G = 1/2 q^T C sigma (A20; Eq. 5-6)."""
+    idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)
+    if len(cq) == 0:
+        return np.zeros(len(idx))
+    return _cdirect.pot_sum(pan.centroid[idx], None, np.asarray(cxyz, np.float64), np.asarray(cq, np.float64), None)
 
 
 def mean_curvature(pan: Panels):
@@ -134,24 +144,44 @@ def self_term_diag(pan: Panels):
     return -mean_curvature(pan) * np.sqrt(pan.area / np.pi) / 4.0
 
 
+class KprimeRows:
+    """O4 split in two: the source weights x_j A_j w_g (once per x) and then any rows i of
+    (K'x)_i = sum_{j!=i} x_j A_j sum_g w_g dG/dn_i(c_i, y_jg) -- the same sums
+    as apply_kprime, so that a timing of rows measures the direct sums only."""
+
+    def __init__(self, pan: Panels, x):
+        self.pan = pan
+        self.y, self.owner, aw = pan.sources()
+        self.w = np.repeat(np.asarray(x, np.float64), pan.K) * aw
+        self.y = np.ascontiguousarray(self.y)
+
+    def __call__(self, rows):
+        idx = np.asarray(rows, np.int64)
+        return _cdirect.dn_sum(self.pan.centroid[idx], self.pan.normal[idx], idx, self.y, self.w, self.owner)
+
+
 def apply_kprime(pan: Panels, x, rows=None, self_term: bool = False):
     """O4: (K'x)_i = sum_{j!=i} x_j A_j sum_g w_g dG/dn_i(c_i, y_jg); K'_ii = 0 (P:326-327, S:364),
     or K'_ii = self_term_diag (option self_term = 1)."""
-    y, owner, aw = pan.sources()
-    w = np.repeat(np.asarray(x, np.float64), pan.K) * aw
     idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)
-    out = _cdirect.dn_sum(pan.centroid[idx], pan.normal[idx], idx, y, w, owner)
+    out = KprimeRows(pan, x)(idx)
     if self_term:
         out = out + self_term_diag(pan)[idx] * np.asarray(x, np.float64)[idx]
     return out
 
 
+class SingleRows(KprimeRows):
+    """O5 split like KprimeRows: (Vx)_i = sum_{j!=i} x_j A_j sum_g w_g G(c_i, y_jg) for any rows."""
+
+    def __call__(self, rows):
+        idx = np.asarray(rows, np.int64)
+        return _cdirect.pot_sum(self.pan.centroid[idx], idx, self.y, self.w, self.owner)
+
+
 def apply_single(pan: Panels, x, rows=None):
     """O5: (Vx)_i = sum_{j!=i} x_j A_j sum_g w_g G(c_i, y_jg)  (Eq. 5)."""
-    y, owner, aw = pan.sources()
-    w = np.repeat(np.asarray(x, np.float64), pan.K) * aw
     idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)
-    return _cdirect.pot_sum(pan.centroid[idx], idx, y, w, owner)
+    return SingleRows(pan, x)(idx)
 
 
 def near_pairs(pan: Panels, eta: float):

@@ -33,7 +33,7 @@ class Options(C.Structure):
                 ("quad_points", C.c_int32), ("near_mode", C.c_int32), ("near_radius", C.c_float),
                 ("self_term", C.c_int32), ("direct", C.c_int32), ("deterministic", C.c_int32),
                 ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("input_mode", C.c_int32)]
 
 
 class SolveOptions(C.Structure):
@@ -48,7 +48,8 @@ class Energy(C.Structure):
 
 class Timing(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("tree", "upward", "m2l", "p2p", "l2p", "near", "comm", "gmres",
-                                          "total")] + [("p2p_interactions", C.c_int64), ("m2l_pairs", C.c_int64)]
+                                          "total")] + [("p2p_interactions", C.c_int64), ("m2l_pairs", C.c_int64)] + \
+        [(k, C.c_double) for k in ("p2m", "m2m", "l2l", "leaf_l2p", "bibee")]
 
 
 class TreeInfo(C.Structure):
@@ -58,7 +59,11 @@ class TreeInfo(C.Structure):
 
 
 # symbol -> (restype, argtypes); every entry point declared in include/fmmbem.h
+ABI_VERSION = 2  # include/fmmbem.h FMMBEM_ABI_VERSION this binding is written for
+
 SIGNATURES = {
+    "fmmbem_abi_version": (C.c_int32, []),
+    "fmmbem_struct_size": (C.c_int64, [C.c_char_p]),
     "fmmbem_default_options": (C.c_int, [C.POINTER(Options)]),
     "fmmbem_get_unique_id": (C.c_int, [C.c_void_p]),
     "fmmbem_split_costs": (C.c_int, [C.POINTER(C.c_double), C.c_int64, C.c_int32, C.POINTER(C.c_int64)]),
@@ -73,10 +78,15 @@ SIGNATURES = {
                                C.POINTER(C.c_double), C.POINTER(Energy)]),
     "fmmbem_bibee_energy": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(Energy)]),
     "fmmbem_charge_fields": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "fmmbem_reset_fields": (C.c_int, [C.c_void_p]),
     "fmmbem_reaction_potential": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
     "fmmbem_last_timing": (C.c_int, [C.c_void_p, C.POINTER(Timing)]),
     "fmmbem_tree_info_get": (C.c_int, [C.c_void_p, C.POINTER(TreeInfo)]),
     "fmmbem_last_error": (C.c_char_p, []),
+    "fmmbem_plan_create": (C.c_int, [C.POINTER(C.c_uint64), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int64,
+                                     C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "fmmbem_plan_destroy": (None, [C.c_void_p]),
+    "fmmbem_plan_list": (C.c_int64, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
 }
 
 _lib = None
@@ -94,6 +104,12 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.fmmbem_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH}: ABI version {lib.fmmbem_abi_version()}, binding expects {ABI_VERSION}")
+    for nm, st in (("options", Options), ("timing", Timing), ("energy", Energy), ("tree_info", TreeInfo),
+                   ("solve_options", SolveOptions)):
+        if lib.fmmbem_struct_size(nm.encode()) != C.sizeof(st):
+            raise ImportError(f"{LIB_PATH}: sizeof({nm}) differs from the binding's ctypes struct")
     _lib = lib
     return lib
 

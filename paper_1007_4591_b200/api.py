@@ -91,7 +91,9 @@ class Solver:
     @classmethod
     def distributed(cls, cfg, group=None, **options):
         """One rank of a multi-GPU solver; torch.distributed must be initialised.  Rank 0 draws the
-        NCCL id and torch.distributed broadcasts it; every rank passes the full problem."""
+        NCCL id and torch.distributed broadcasts it.  input_mode 0 (default): every rank passes the
+        full problem; input_mode=1: `cfg` holds only this rank's part of the mesh (all charges), see
+        include/fmmbem.h."""
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         obj = [get_unique_id() if rank == 0 else None]
@@ -132,13 +134,33 @@ class Solver:
             raise ValueError(f"vector of {x.numel()} entries, expected {self.n}")
         return x
 
+    def _check_dev(self, t, what):
+        """A caller-provided device buffer the library writes or reads in place: float32,
+        contiguous, n entries, on this ctx's device (the ABI takes a raw pointer)."""
+        torch = self._torch
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{what} must be a torch tensor")
+        if t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != self.n or t.device != self._dev():
+            raise ValueError(f"{what} must be a contiguous float32 tensor of {self.n} entries on {self._dev()}")
+        return t
+
+    def _sync_current(self):
+        # blocking ABI calls run on the library's own stream: finish the caller's pending work on
+        # the buffers they read or write first (include/fmmbem.h "Ordering")
+        self._torch.cuda.current_stream(self._dev()).synchronize()
+
     # ---- ABI calls
     def matvec(self, x, op="kprime", out=None, stream=None):
         """y = op(x) on the GPU (local order); x: torch CUDA float32 tensor or array."""
         torch = self._torch
         x = self._vec(x)
-        y = torch.empty_like(x) if out is None else out
-        st = torch.cuda.current_stream(self._dev()) if stream is None else stream
+        y = torch.empty_like(x) if out is None else self._check_dev(out, "out")
+        cur = torch.cuda.current_stream(self._dev())
+        st = cur if stream is None else stream
+        if st != cur:  # the kernels read x / write y on st: keep the allocator from recycling them early
+            st.wait_stream(cur)
+            x.record_stream(st)
+            y.record_stream(st)
         L.check(self.lib.fmmbem_matvec(self._h, OPS[op], C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
                                        C.c_void_p(st.cuda_stream)))
         return y
@@ -146,7 +168,15 @@ class Solver:
     def matvec_host(self, x_host, op="kprime", y_host=None):
         """End-to-end product with host buffers (copies inside the library)."""
         x = np.ascontiguousarray(x_host, np.float32)
-        y = np.empty_like(x) if y_host is None else y_host
+        if x.size != self.n:
+            raise ValueError(f"x_host has {x.size} entries, expected {self.n}")
+        if y_host is None:
+            y = np.empty_like(x)
+        else:
+            y = y_host
+            if not (isinstance(y, np.ndarray) and y.dtype == np.float32 and y.flags.c_contiguous
+                    and y.size == self.n and y.flags.writeable):
+                raise ValueError(f"y_host must be a writeable contiguous float32 array of {self.n} entries")
         L.check(self.lib.fmmbem_matvec_host(self._h, OPS[op], C.c_void_p(x.ctypes.data),
                                             C.c_void_p(y.ctypes.data)))
         return y
@@ -155,13 +185,19 @@ class Solver:
         torch = self._torch
         En = torch.empty(self.n, device=self._dev(), dtype=torch.float32)
         psi = torch.empty_like(En)
+        self._sync_current()
         L.check(self.lib.fmmbem_charge_fields(self._h, C.c_void_p(En.data_ptr()), C.c_void_p(psi.data_ptr())))
         return En, psi
+
+    def reset_fields(self):
+        """Drop the cached charge-FMM fields (the next bibee / solve recomputes E_n and psi)."""
+        L.check(self.lib.fmmbem_reset_fields(self._h))
 
     def bibee(self, variant="cfa", want_sigma=False):
         torch = self._torch
         e = L.Energy()
         sig = torch.empty(self.n, device=self._dev(), dtype=torch.float32) if want_sigma else None
+        self._sync_current()
         L.check(self.lib.fmmbem_bibee_energy(self._h, BIBEE[variant],
                                              C.c_void_p(sig.data_ptr()) if sig is not None else None, C.byref(e)))
         out = dict(dG=e.dG_internal, dG_kcal=e.dG_kcal_mol)
@@ -171,10 +207,13 @@ class Solver:
 
     def solve(self, tol=1e-6, restart=30, max_iters=200, x0=None):
         torch = self._torch
+        if x0 is not None:
+            x0 = self._check_dev(x0, "x0")
         so = L.SolveOptions(tol, restart, max_iters, C.c_void_p(x0.data_ptr()) if x0 is not None else None)
         sig = torch.empty(self.n, device=self._dev(), dtype=torch.float32)
         hist = np.empty(max_iters + 1, np.float64)
         e = L.Energy()
+        self._sync_current()
         code = L.check(self.lib.fmmbem_solve(self._h, C.byref(so), C.c_void_p(sig.data_ptr()),
                                              hist.ctypes.data_as(C.POINTER(C.c_double)), C.byref(e)))
         return dict(sigma=sig, dG=e.dG_internal, dG_kcal=e.dG_kcal_mol, iterations=e.iterations,
@@ -183,6 +222,7 @@ class Solver:
     def reaction_potential(self, sigma):
         sigma = self._vec(sigma)
         phi = np.empty(self.n_charges, np.float64)
+        self._sync_current()
         L.check(self.lib.fmmbem_reaction_potential(self._h, C.c_void_p(sigma.data_ptr()), _dp(phi)))
         return phi
 

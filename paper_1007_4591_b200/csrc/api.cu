@@ -2,6 +2,7 @@
 // evaluation.  Every step of the path runs in this library's kernels;
 // the host only validates, launches and runs the small FP64 GMRES least-squares problem.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -47,26 +48,32 @@ void quad_rule(int K, std::vector<double>& beta, std::vector<double>& w) {
 }
 
 // Panel prep: FP64 centroid, unit normal from
-// the winding, area, quadrature points; flags index-out-of-range and degenerate triangles.
+// the winding, area, quadrature points.  Bad triangles are flagged by the smallest offending index
+// per kind: bad[0] vertex index out of range, bad[1] non-finite vertex, bad[2] degenerate.
 __global__ void k_prep(int64_t np, int64_t nv, const double* __restrict__ V, const int* __restrict__ T, int K,
                        const double* __restrict__ beta, double atol, double* cen, double* nrm, double* area,
-                       double* qp, int* bad) {
+                       double* qp, unsigned long long* bad) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= np) return;
   int a = T[3 * i], b = T[3 * i + 1], c = T[3 * i + 2];
   if (a < 0 || b < 0 || c < 0 || a >= nv || b >= nv || c >= nv) {
-    atomicMin(bad, (int)i);
+    atomicMin(&bad[0], (unsigned long long)i);
     return;
   }
   const double* A = V + 3 * (int64_t)a;
   const double* B = V + 3 * (int64_t)b;
   const double* C = V + 3 * (int64_t)c;
+  for (int d = 0; d < 3; ++d)
+    if (!isfinite(A[d]) || !isfinite(B[d]) || !isfinite(C[d])) {
+      atomicMin(&bad[1], (unsigned long long)i);
+      return;
+    }
   double e1[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
   double e2[3] = {C[0] - A[0], C[1] - A[1], C[2] - A[2]};
   double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
   double nn = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
   if (!(0.5 * nn >= atol)) {
-    atomicMin(bad, (int)i);
+    atomicMin(&bad[2], (unsigned long long)i);
     return;
   }
   for (int d = 0; d < 3; ++d) {
@@ -78,6 +85,31 @@ __global__ void k_prep(int64_t np, int64_t nv, const double* __restrict__ V, con
     for (int g = 0; g < K; ++g)
       for (int d = 0; d < 3; ++d)
         qp[(i * K + g) * 3 + d] = beta[3 * g] * A[d] + beta[3 * g + 1] * B[d] + beta[3 * g + 2] * C[d];
+}
+
+// bounding box of the finite vertex coordinates: out = (min xyz, -max xyz) per block
+__global__ void k_vbox(int64_t n, const double* __restrict__ V, double* out) {
+  double v[6] = {1e300, 1e300, 1e300, 1e300, 1e300, 1e300};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < 3; ++d) {
+      const double x = V[3 * i + d];
+      if (isfinite(x)) {
+        v[d] = fmin(v[d], x);
+        v[3 + d] = fmin(v[3 + d], -x);
+      }
+    }
+  for (int k = 0; k < 6; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] = fmin(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+  __shared__ double sh[8][6];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 6; ++k) sh[w][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double r = 1e300;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmin(r, sh[i][threadIdx.x]);
+    out[blockIdx.x * 6 + threadIdx.x] = r;
+  }
 }
 
 __global__ void k_scale(float* y, const float* x, int64_t n, float s) {
@@ -113,53 +145,27 @@ struct DevGuard {
   }
 };
 
-// leaf cost for the partition: P2P interactions + M2L translations (~600 interaction-equivalents
-// each at P = 12) + per-point work
-__global__ void k_leaf_cost(int nl, int leaf_cell0, const int* __restrict__ tbeg, const int* __restrict__ off,
-                            const int* __restrict__ idx, const int* __restrict__ m2l_off, double* cost,
-                            long long* p2p) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nl) return;
-  long long nt = tbeg[k + 1] - tbeg[k], s = 0;
-  for (int e = off[k]; e < off[k + 1]; ++e) s += tbeg[idx[e] + 1] - tbeg[idx[e]];
-  const int cell = leaf_cell0 + k;
-  const double m2l = (double)(m2l_off[cell + 1] - m2l_off[cell]);
-  p2p[k] = nt * s;
-  cost[k] = (double)(nt * s) + (nt ? 600.0 * m2l : 0.0) + 50.0 * (double)nt;
-}
-
-__global__ void k_own_leaf_counts(int nl, const int* __restrict__ begin, int mult, int leaf_off, int lo, int hi,
-                                  int* cnt) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < nl) cnt[leaf_off + k] = (k >= lo && k < hi) ? (begin[k + 1] - begin[k]) * mult : 0;
-}
-
-__global__ void k_up_counts2(int n, int off, const int* __restrict__ cb, const int* __restrict__ ce, int* cnt) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int s = 0;
-  for (int c = cb[off + i]; c < ce[off + i]; ++c) s += cnt[c];
-  cnt[off + i] = s;
-}
+// Stream ordering between entry points (the library's internal state -- expansions, staging
+// buffers, the P2P source table -- is shared by every call): each call first makes the stream it
+// runs on wait for the end of the previous call, and records c->done when its own work is queued.
+void order_after_last(fmmbem_ctx* c, cudaStream_t st) { FMM_CUDA(cudaStreamWaitEvent(st, c->done, 0)); }
+void mark_done(fmmbem_ctx* c, cudaStream_t st) { FMM_CUDA(cudaEventRecord(c->done, st)); }
 
 bool multi(const fmmbem_ctx* c) { return c->nranks > 1; }
 
-// Sources of the panel operators (K', V, A): x_local is this rank's slice; with nranks > 1 it is
-// all-gathered (P2P needs the neighbours' weights) and P2M runs on the owned leaves only.
+// Sources of the panel operators (K', V, A): x_local is this rank's slice.  With nranks > 1 the
+// source weights live in c->xext = [halo | owned | halo] (local point indices): the owned slice is
+// copied in here (before the far-field fork: P2M reads it), the peers' halo weights arrive by the
+// grouped send / recv fmm_eval issues on the caller's stream for the near field (P2P).
 SrcArg kp_src(fmmbem_ctx* c, const float* x_local, cudaStream_t st, bool* distributed) {
   SrcArg s;
   s.set = (c->K == 1) ? &c->pan : &c->quad;
   s.x = x_local;
   *distributed = false;
   if (multi(c)) {
-    c->xfull.alloc(c->np);
-    s.x = c->xfull.get();
-    s.x_far = x_local - c->pan_lo;  // P2M reads owned panels only: a global-index view of the slice
-    if (c->overlap && c->comm2) {
-      s.ag_src = x_local;  // all-gathered by fmm_eval on the caller's stream, behind the fork
-    } else {
-      comm_allgatherv_f32(c, x_local, c->xfull.get(), c->pan_offs, st);
-    }
+    halo_copy_owned(c, x_local, st);
+    s.x = c->xext.get();
+    s.halo_src = x_local;
     s.leaf_lo = c->leaf_lo;
     s.leaf_hi = c->leaf_hi;
     s.cnt = (c->K == 1) ? c->pan_own_cnt.get() : c->quad_own_cnt.get();
@@ -184,7 +190,7 @@ TgtArg own_targets(fmmbem_ctx* c, bool quad) {
 
 enum : int {
   E_START = 0, E_UP0, E_UP1, E_AR0, E_AR1, E_M2L0, E_M2L1, E_DN1, E_P2P0, E_P2P1, E_L2P0, E_L2P1, E_AG0, E_AG1,
-  E_NEAR1, E_XG0, E_XG1, E_END
+  E_NEAR1, E_XG0, E_XG1, E_P2M1, E_L2L1, E_BIB0, E_BIB1, E_END
 };
 
 // Option self_term = 1: K'_ii = -H_i sqrt(A_i / pi) / 4, the principal-value integral of
@@ -217,8 +223,9 @@ void build_self_term(fmmbem_ctx* c, const fmmbem_mesh* mesh, cudaStream_t s) {
     if (l > 0)
       for (int d = 0; d < 3; ++d) vn[3 * v + d] /= l;
   }
-  std::vector<float> dl(np);
-  for (int64_t k = 0; k < np; ++k) {
+  const int64_t nloc = c->pan.n;  // local points (owned + halo), pan_ids = their global triangle ids
+  std::vector<float> dl(nloc);
+  for (int64_t k = 0; k < nloc; ++k) {
     const int64_t t = c->pan_ids[k];
     double H = 0.0;
     for (int j = 0; j < 3; ++j) {
@@ -234,8 +241,8 @@ void build_self_term(fmmbem_ctx* c, const fmmbem_mesh* mesh, cudaStream_t s) {
     H /= 3.0;
     dl[k] = (float)(-H * std::sqrt(area[t] / M_PI) / 4.0 * 4.0 * M_PI);
   }
-  c->selfd.alloc(np);
-  FMM_CUDA(cudaMemcpyAsync(c->selfd.get(), dl.data(), np * sizeof(float), cudaMemcpyHostToDevice, s));
+  c->selfd.alloc(std::max<int64_t>(nloc, 1));
+  if (nloc) FMM_CUDA(cudaMemcpyAsync(c->selfd.get(), dl.data(), nloc * sizeof(float), cudaMemcpyHostToDevice, s));
   FMM_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -260,9 +267,11 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
   }
   if (!direct) {
     rec(E_UP0, fs);
-    SrcArg sf = s;
-    if (s.x_far) sf.x = s.x_far;
-    launch_upward(c, sf, fs);
+    const SrcArg& sf = s;
+    c->Mx.zero(fs);  // the upward sweep, split for the phase events: P2M, then M2M level by level
+    launch_p2m_range(c, sf, sf.leaf_lo, sf.leaf_hi < 0 ? (int)c->tree.n_leaves : sf.leaf_hi, fs);
+    rec(E_P2M1, fs);
+    launch_m2m_levels(c, sf, fs);
     rec(E_UP1, fs);
     if (distributed) {  // the multipoles this rank's interaction lists need (LET)
       rec(E_AR0, fs);
@@ -280,11 +289,12 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     rec(E_M2L1, fs);
     launch_downward(c, tcnt, fs);
     rec(E_DN1, fs);
+    rec(E_L2L1, fs);
   }
   if (ovl) FMM_CUDA(cudaEventRecord(c->join, fs));
-  if (s.ag_src) {  // x slices of the other ranks for the near field, overlapped with the far chain
+  if (s.halo_src) {  // the peers' halo weights for the near field, overlapped with the far chain
     rec(E_XG0, st);
-    comm_allgatherv_f32(c, s.ag_src, const_cast<float*>(s.x), c->pan_offs, st, /*second=*/true);
+    halo_exchange(c, s.halo_src, st);
     rec(E_XG1, st);
   }
   rec(E_P2P0, st);
@@ -300,7 +310,7 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
   }
   rec(E_L2P1, st);
   c->timed_comm = timing && distributed && !direct;
-  c->timed_xg = timing && s.ag_src != nullptr;
+  c->timed_xg = timing && s.halo_src != nullptr;
 }
 
 // y = op(x) on this rank's panels; x, y local slices (pointers are shifted so that the kernels'
@@ -331,24 +341,7 @@ void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_
   TgtArg t = own_targets(c, false);
   float* yg = y - c->pan_lo;
   const float* xg = x - c->pan_lo;
-  Outputs o;
-  if (op == FMMBEM_OP_SINGLE) {
-    o.pot.y = yg;
-    o.pot.b = (float)(1.0 / FOUR_PI);
-  } else {
-    o.dn.y = yg;
-    if (op == FMMBEM_OP_KPRIME) {
-      o.dn.b = (float)(1.0 / FOUR_PI);
-    } else {  // A = I - f K'
-      o.dn.x = xg;
-      o.dn.ax = 1.f;
-      o.dn.b = (float)(-c->f / FOUR_PI);
-    }
-    if (c->selfd.n) {  // K'_ii = d_i (stored times 4 pi, like the raw kernel sums)
-      o.dn.x = xg;
-      o.dn.d = c->selfd.get();
-    }
-  }
+  Outputs o = op_outputs(c, op, xg, yg);
   bool dist = false;
   if (timing) cudaEventRecord(c->ev[E_AG0], st);
   SrcArg s = kp_src(c, x, st, &dist);
@@ -410,63 +403,13 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
   c->have_fields = true;
 }
 
-// Multi-GPU partition: contiguous Morton ranges of leaves with equal estimated cost
-// ("equally distribute the Morton-indexed boxes", weighted by work instead of count).
-void partition(fmmbem_ctx* c, cudaStream_t st) {
-  const Tree& T = c->tree;
-  const int nl = (int)T.n_leaves;
-  DevBuf<double> cost;
-  DevBuf<long long> p2p;
-  cost.alloc(std::max(nl, 1));
-  p2p.alloc(std::max(nl, 1));
-  const PointSet& S = (c->K == 1) ? c->pan : c->quad;
-  k_leaf_cost<<<ceil_div(nl, 256), 256, 0, st>>>(nl, (int)T.lvl_off[T.L], c->pan.begin.get(), T.nbr_off.get(),
-                                                 T.nbr_idx.get(), T.m2l_off.get(), cost.get(), p2p.get());
-  FMM_CHECK_LAUNCH();
-  (void)S;
-  std::vector<double> hc(nl);
-  std::vector<long long> hp(nl);
-  std::vector<int> beg(nl + 1);
-  FMM_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), nl * sizeof(double), cudaMemcpyDeviceToHost, st));
-  FMM_CUDA(cudaMemcpyAsync(hp.data(), p2p.get(), nl * sizeof(long long), cudaMemcpyDeviceToHost, st));
-  FMM_CUDA(cudaMemcpyAsync(beg.data(), c->pan.begin.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
-  FMM_CUDA(cudaStreamSynchronize(st));
-  const int R = c->nranks;
-  std::vector<int64_t> bounds(R + 1);
-  split_costs(hc.data(), nl, R, bounds.data());
-  c->leaf_bounds = bounds;
-  c->leaf_lo = (int)bounds[c->rank];
-  c->leaf_hi = (int)bounds[c->rank + 1];
-  c->pan_offs.assign(R + 1, 0);
-  for (int r = 0; r <= R; ++r) c->pan_offs[r] = beg[bounds[r]];
-  c->pan_lo = c->pan_offs[c->rank];
-  c->pan_hi = c->pan_offs[c->rank + 1];
-  long long own = 0;
-  for (int k = c->leaf_lo; k < c->leaf_hi; ++k) own += hp[k];
-  c->p2p_inter_kp = own - (int64_t)c->n_own() * (c->K == 1 ? 1 : c->K);
-  // subtree counts of the owned points
-  for (int q = 0; q < 2; ++q) {
-    if (q == 1 && c->K == 1) continue;
-    DevBuf<int>& cnt = q ? c->quad_own_cnt : c->pan_own_cnt;
-    cnt.alloc(T.n_cells);
-    cnt.zero(st);
-    k_own_leaf_counts<<<ceil_div(nl, 256), 256, 0, st>>>(nl, c->pan.begin.get(), q ? c->K : 1, (int)T.lvl_off[T.L],
-                                                         c->leaf_lo, c->leaf_hi, cnt.get());
-    for (int l = T.L - 1; l >= 0; --l) {
-      int n = (int)(T.lvl_off[l + 1] - T.lvl_off[l]);
-      k_up_counts2<<<ceil_div(n, 256), 256, 0, st>>>(n, (int)T.lvl_off[l], T.child_begin.get(), T.child_end.get(),
-                                                     cnt.get());
-    }
-    FMM_CHECK_LAUNCH();
-  }
-  FMM_CUDA(cudaStreamSynchronize(st));
-}
-
 void fill_timing(fmmbem_ctx* c, bool direct) {
   fmmbem_timing& T = c->last;
-  const double g = T.gmres;
+  const double g = T.gmres, tr = T.tree, bb = T.bibee;
   std::memset(&T, 0, sizeof(T));
   T.gmres = g;
+  T.tree = tr;
+  T.bibee = bb;
   if (!c->timed_near) return;
   cudaEventSynchronize(c->ev[E_NEAR1]);
   auto el = [&](int a, int b) {
@@ -475,8 +418,12 @@ void fill_timing(fmmbem_ctx* c, bool direct) {
   };
   if (!direct) {
     T.upward = el(E_UP0, E_UP1);
+    T.p2m = el(E_UP0, E_P2M1);
+    T.m2m = el(E_P2M1, E_UP1);
     T.m2l = el(E_M2L0, E_M2L1);
-    T.l2p = el(E_M2L1, E_DN1) + el(E_L2P0, E_L2P1);  // L2L + L2P
+    T.l2l = el(E_M2L1, E_DN1);
+    T.leaf_l2p = el(E_L2P0, E_L2P1);
+    T.l2p = T.l2l + T.leaf_l2p;
   }
   T.p2p = el(E_P2P0, E_P2P1);
   T.near = el(E_L2P1, E_NEAR1);
@@ -506,6 +453,19 @@ extern "C" {
 
 const char* fmmbem_last_error(void) { return g_err.c_str(); }
 
+int32_t fmmbem_abi_version(void) { return FMMBEM_ABI_VERSION; }
+
+int64_t fmmbem_struct_size(const char* name) {
+  if (!name) return -1;
+  const std::string n(name);
+  if (n == "options") return sizeof(fmmbem_options);
+  if (n == "timing") return sizeof(fmmbem_timing);
+  if (n == "energy") return sizeof(fmmbem_energy);
+  if (n == "tree_info") return sizeof(fmmbem_tree_info);
+  if (n == "solve_options") return sizeof(fmmbem_solve_options);
+  return -1;
+}
+
 fmmbem_status fmmbem_default_options(fmmbem_options* o) {
   if (!o) return FMMBEM_E_INVALID;
   std::memset(o, 0, sizeof(*o));
@@ -522,6 +482,7 @@ fmmbem_status fmmbem_default_options(fmmbem_options* o) {
   o->rank = 0;
   o->nranks = 1;
   o->nccl_id = nullptr;
+  o->input_mode = 0;
   return FMMBEM_OK;
 }
 
@@ -544,19 +505,23 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   if (opt.near_mode != 0 && opt.near_mode != 1) throw Error(FMMBEM_E_INVALID, "near_mode must be 0 or 1");
   if (opt.near_mode == 1 && !(opt.near_radius > 0.f)) throw Error(FMMBEM_E_INVALID, "near_radius must be > 0");
   if (opt.self_term != 0 && opt.self_term != 1) throw Error(FMMBEM_E_INVALID, "self_term must be 0 or 1");
-  if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks) throw Error(FMMBEM_E_INVALID, "bad rank / nranks");
+  if (opt.nranks < 1 || opt.nranks > 64 || opt.rank < 0 || opt.rank >= opt.nranks)
+    throw Error(FMMBEM_E_INVALID, "bad rank / nranks (1..64 ranks)");
   if (opt.nranks > 1 && !opt.nccl_id) throw Error(FMMBEM_E_INVALID, "nranks > 1 needs options.nccl_id");
   if (opt.nranks > 1 && opt.direct) throw Error(FMMBEM_E_INVALID, "direct mode is single-GPU only");
+  if (opt.input_mode != 0 && opt.input_mode != 1) throw Error(FMMBEM_E_INVALID, "input_mode must be 0 or 1");
+  const bool parts = opt.nranks > 1 && opt.input_mode == 1;
+  if (parts && (opt.near_mode || opt.self_term))
+    throw Error(FMMBEM_E_INVALID, "near_mode / self_term need the full mesh on every rank (input_mode 0)");
   if (!(eps_in > 0) || !(eps_out > 0) || eps_in == eps_out || !std::isfinite(eps_in) || !std::isfinite(eps_out))
     throw Error(FMMBEM_E_INVALID, "need eps_in, eps_out > 0 and eps_in != eps_out");
-  if (mesh->n_triangles < 1 || mesh->n_vertices < 3 || !mesh->xyz || !mesh->tri)
-    throw Error(FMMBEM_E_INVALID, "empty mesh");
+  if (mesh->n_triangles < 0 || mesh->n_vertices < 0 || (mesh->n_triangles > 0 && (!mesh->xyz || !mesh->tri)))
+    throw Error(FMMBEM_E_INVALID, "bad mesh arrays");
+  if (!parts && (mesh->n_triangles < 1 || mesh->n_vertices < 3)) throw Error(FMMBEM_E_INVALID, "empty mesh");
   const int64_t nc = chg ? chg->n : 0;
   if (nc < 0 || (nc > 0 && (!chg->xyz || !chg->q))) throw Error(FMMBEM_E_INVALID, "bad charges");
   if (mesh->n_triangles * (int64_t)opt.quad_points >= (1LL << 31) || mesh->n_vertices >= (1LL << 31))
     throw Error(FMMBEM_E_INVALID, "problem too large for 32-bit point indices");
-  for (int64_t i = 0; i < 3 * mesh->n_vertices; ++i)
-    if (!std::isfinite(mesh->xyz[i])) throw Error(FMMBEM_E_INVALID, "non-finite vertex " + std::to_string(i / 3));
   for (int64_t i = 0; i < nc; ++i) {
     if (!std::isfinite(chg->q[i]) || !std::isfinite(chg->xyz[3 * i]) || !std::isfinite(chg->xyz[3 * i + 1]) ||
         !std::isfinite(chg->xyz[3 * i + 2]))
@@ -576,6 +541,7 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   for (auto& e : c->ev) FMM_CUDA(cudaEventCreate(&e));
   FMM_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
   c->P = opt.terms;
   if (const char* e = std::getenv("FMMBEM_M2L")) c->m2l_mode = (std::string(e) == "p4") ? 1 : 0;
   if (const char* e = std::getenv("FMMBEM_P2P_CHUNK")) c->p2p_chunk = std::max(8, std::min(256, std::atoi(e)));
@@ -591,49 +557,107 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   c->eps_out = eps_out;
   c->f = 2.0 * (eps_out - eps_in) / (eps_in + eps_out);  // reading A1
   c->eps_hat = 1.0 - eps_in / eps_out;
-  c->np = mesh->n_triangles;
   c->nc = nc;
+  c->rank = opt.rank;
+  c->nranks = opt.nranks;
   cudaStream_t s = c->stream;
-  const int64_t np = c->np, nv = mesh->n_vertices;
-  // upload + panel prep
+  if (c->nranks > 1) comm_init(c, opt.nccl_id);
+  const int R = c->nranks, me = c->rank;
+  // this rank's input slice: input_mode 0 = [r n / R, (r + 1) n / R) of the full mesh every rank
+  // passes; input_mode 1 = the rank's own panels, global ids after those of the lower ranks
+  const int64_t nt = mesh->n_triangles, nv = mesh->n_vertices;
+  int64_t t0 = 0, m = nt;
+  if (R > 1 && !parts) {
+    t0 = nt * me / R;
+    m = nt * (me + 1) / R - t0;
+  }
+  int64_t gid0 = t0;
+  if (parts) {
+    DevBuf<int64_t> mine, all;
+    mine.alloc(1);
+    all.alloc(R);
+    FMM_CUDA(cudaMemcpyAsync(mine.get(), &m, sizeof(m), cudaMemcpyHostToDevice, s));
+    comm_allgather_i64(c, mine.get(), all.get(), 1, s);
+    std::vector<int64_t> h(R);
+    FMM_CUDA(cudaMemcpyAsync(h.data(), all.get(), R * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    gid0 = 0;
+    int64_t tot = 0;
+    for (int r = 0; r < R; ++r) {
+      if (r < me) gid0 += h[r];
+      tot += h[r];
+    }
+    if (tot < 1) throw Error(FMMBEM_E_INVALID, "empty mesh");
+  }
+  // upload + panel prep (FP64) of the slice
   DevBuf<double> dV, cen, nrm, area, qp, beta, wq, cx, cq;
   DevBuf<int> dT;
-  dV.alloc(3 * nv);
-  dT.alloc(3 * np);
-  FMM_CUDA(cudaMemcpyAsync(dV.get(), mesh->xyz, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, s));
-  FMM_CUDA(cudaMemcpyAsync(dT.get(), mesh->tri, 3 * np * sizeof(int), cudaMemcpyHostToDevice, s));
+  dV.alloc(std::max<int64_t>(3 * nv, 1));
+  dT.alloc(std::max<int64_t>(3 * m, 1));
+  if (nv) FMM_CUDA(cudaMemcpyAsync(dV.get(), mesh->xyz, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (m) FMM_CUDA(cudaMemcpyAsync(dT.get(), mesh->tri + 3 * t0, 3 * m * sizeof(int), cudaMemcpyHostToDevice, s));
   std::vector<double> hb, hw;
   quad_rule(c->K, hb, hw);
   beta.alloc(hb.size());
   wq.alloc(hw.size());
   FMM_CUDA(cudaMemcpyAsync(beta.get(), hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   FMM_CUDA(cudaMemcpyAsync(wq.get(), hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
-  for (int64_t i = 0; i < nv; ++i)
-    for (int d = 0; d < 3; ++d) {
-      mn[d] = std::min(mn[d], mesh->xyz[3 * i + d]);
-      mx[d] = std::max(mx[d], mesh->xyz[3 * i + d]);
+  // degeneracy tolerance 1e-14 bbox_diag^2 from the vertex bounding box of all ranks
+  double box[6] = {1e300, 1e300, 1e300, 1e300, 1e300, 1e300};
+  {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (nv + 255) / 256));
+    DevBuf<double> part;
+    part.alloc(blocks * 6);
+    k_vbox<<<blocks, 256, 0, s>>>(nv, dV.get(), part.get());
+    FMM_CHECK_LAUNCH();
+    std::vector<double> h(blocks * 6);
+    FMM_CUDA(cudaMemcpyAsync(h.data(), part.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    for (int b = 0; b < blocks; ++b)
+      for (int k = 0; k < 6; ++k) box[k] = std::min(box[k], h[b * 6 + k]);
+    if (parts) {
+      DevBuf<double> d;
+      d.alloc(6);
+      FMM_CUDA(cudaMemcpyAsync(d.get(), box, sizeof(box), cudaMemcpyHostToDevice, s));
+      comm_allreduce_f64_op(c, d.get(), 6, -1, s);
+      FMM_CUDA(cudaMemcpyAsync(box, d.get(), sizeof(box), cudaMemcpyDeviceToHost, s));
+      FMM_CUDA(cudaStreamSynchronize(s));
     }
+  }
   double diag2 = 0;
-  for (int d = 0; d < 3; ++d) diag2 += (mx[d] - mn[d]) * (mx[d] - mn[d]);
-  cen.alloc(3 * np);
-  nrm.alloc(3 * np);
-  area.alloc(np);
-  if (c->K > 1) qp.alloc(3 * np * c->K);
-  c->flag.alloc(4);
-  int big = 0x7fffffff;
-  FMM_CUDA(cudaMemcpyAsync(c->flag.get(), &big, sizeof(int), cudaMemcpyHostToDevice, s));
-  k_prep<<<ceil_div(np, 256), 256, 0, s>>>(np, nv, dV.get(), dT.get(), c->K, beta.get(), 1e-14 * diag2, cen.get(),
-                                           nrm.get(), area.get(), c->K > 1 ? qp.get() : nullptr, c->flag.get());
-  FMM_CHECK_LAUNCH();
-  int bad = 0;
-  FMM_CUDA(cudaMemcpyAsync(&bad, c->flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  FMM_CUDA(cudaStreamSynchronize(s));
-  if (bad != big) {
-    const int* t = mesh->tri + 3 * (int64_t)bad;
-    bool range = t[0] < 0 || t[1] < 0 || t[2] < 0 || t[0] >= nv || t[1] >= nv || t[2] >= nv;
-    throw Error(FMMBEM_E_DEGENERATE, std::string(range ? "triangle index out of range" : "degenerate triangle") +
-                                         " " + std::to_string(bad));
+  for (int d = 0; d < 3; ++d) {
+    const double ext = -box[3 + d] - box[d];
+    if (ext > 0 && ext < 1e300) diag2 += ext * ext;
+  }
+  cen.alloc(std::max<int64_t>(3 * m, 1));
+  nrm.alloc(std::max<int64_t>(3 * m, 1));
+  area.alloc(std::max<int64_t>(m, 1));
+  if (c->K > 1) qp.alloc(std::max<int64_t>(3 * m * c->K, 1));
+  {
+    DevBuf<unsigned long long> bad;
+    bad.alloc(3);
+    const unsigned long long none[3] = {~0ULL, ~0ULL, ~0ULL};
+    FMM_CUDA(cudaMemcpyAsync(bad.get(), none, sizeof(none), cudaMemcpyHostToDevice, s));
+    if (m)
+      k_prep<<<ceil_div(m, 256), 256, 0, s>>>(m, nv, dV.get(), dT.get(), c->K, beta.get(), 1e-14 * diag2, cen.get(),
+                                              nrm.get(), area.get(), c->K > 1 ? qp.get() : nullptr, bad.get());
+    FMM_CHECK_LAUNCH();
+    unsigned long long hbad[3];
+    FMM_CUDA(cudaMemcpyAsync(hbad, bad.get(), sizeof(hbad), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    double g[3];  // global triangle id of the first bad triangle of each kind, agreed by every rank
+    for (int k = 0; k < 3; ++k) g[k] = hbad[k] == ~0ULL ? 1e300 : (double)(gid0 + (int64_t)hbad[k]);
+    if (R > 1) {
+      DevBuf<double> d;
+      d.alloc(3);
+      FMM_CUDA(cudaMemcpyAsync(d.get(), g, sizeof(g), cudaMemcpyHostToDevice, s));
+      comm_allreduce_f64_op(c, d.get(), 3, -1, s);
+      FMM_CUDA(cudaMemcpyAsync(g, d.get(), sizeof(g), cudaMemcpyDeviceToHost, s));
+      FMM_CUDA(cudaStreamSynchronize(s));
+    }
+    if (g[0] < 1e300) throw Error(FMMBEM_E_DEGENERATE, "triangle index out of range " + std::to_string((long long)g[0]));
+    if (g[1] < 1e300) throw Error(FMMBEM_E_INVALID, "non-finite vertex in triangle " + std::to_string((long long)g[1]));
+    if (g[2] < 1e300) throw Error(FMMBEM_E_DEGENERATE, "degenerate triangle " + std::to_string((long long)g[2]));
   }
   if (nc) {
     cx.alloc(3 * nc);
@@ -641,33 +665,49 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
     FMM_CUDA(cudaMemcpyAsync(cx.get(), chg->xyz, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, s));
     FMM_CUDA(cudaMemcpyAsync(cq.get(), chg->q, nc * sizeof(double), cudaMemcpyHostToDevice, s));
   }
-  build_tree(c, cen.get(), nrm.get(), area.get(), qp.get(), wq.get(), cx.get(), cq.get(), s);
+  PanelInput pin;
+  pin.n = m;
+  pin.gid0 = gid0;
+  pin.cen = cen.get();
+  pin.nrm = nrm.get();
+  pin.area = area.get();
+  pin.qp = c->K > 1 ? qp.get() : nullptr;
+  const auto t_tree = std::chrono::steady_clock::now();
+  build_tree(c, pin, wq.get(), cx.get(), cq.get(), s);  // synchronises s
+  c->last.tree = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_tree).count();
   init_tables(c);
   c->Mx.alloc((size_t)c->tree.n_cells * c->NC);
   c->Lx.alloc((size_t)c->tree.n_cells * c->NC);
   c->red.alloc(64);
+  c->flag.alloc(4);
   const PointSet& src = (c->K == 1) ? c->pan : c->quad;
-  c->rank = opt.rank;
-  c->nranks = opt.nranks;
-  c->leaf_lo = 0;
-  c->leaf_hi = (int)c->tree.n_leaves;
-  c->pan_lo = 0;
-  c->pan_hi = np;
-  c->pan_offs = {0, np};
-  c->p2p_inter_kp = count_p2p(c, c->pan, src, true, c->opt.direct != 0 || c->tree.L < 2);
-  if (c->nranks > 1) {
-    comm_init(c, opt.nccl_id);
-    partition(c, s);
+  const bool direct = c->opt.direct != 0 || c->tree.L < 2;
+  if (R == 1) c->p2p_inter_kp = count_p2p(c, c->pan, src, true, direct);
+  if (R > 1) {
     const char* e = std::getenv("FMMBEM_LET");
-    if (!(c->opt.direct != 0 || c->tree.L < 2) && !(e && std::atoi(e) == 0)) build_let(c, c->leaf_bounds, s);
+    if (!direct && !(e && std::atoi(e) == 0)) build_let(c, c->leaf_bounds, s);
   }
-  if (c->opt.near_mode == 1) build_near(c, dV.get(), dT.get(), cen.get(), nrm.get(), area.get(), beta.get(), wq.get(), s);
+  if (c->opt.near_mode == 1) {
+    if (R > 1) {  // the analytic near field needs FP64 geometry of every local (owned + halo) panel
+      cen.alloc(3 * nt);
+      nrm.alloc(3 * nt);
+      area.alloc(nt);
+      DevBuf<unsigned long long> bad;
+      bad.alloc(3);
+      dT.alloc(3 * nt);
+      FMM_CUDA(cudaMemcpyAsync(dT.get(), mesh->tri, 3 * nt * sizeof(int), cudaMemcpyHostToDevice, s));
+      k_prep<<<ceil_div(nt, 256), 256, 0, s>>>(nt, nv, dV.get(), dT.get(), 1, beta.get(), 0.0, cen.get(), nrm.get(),
+                                               area.get(), nullptr, bad.get());
+      FMM_CHECK_LAUNCH();
+    }
+    build_near(c, dV.get(), dT.get(), cen.get(), nrm.get(), area.get(), beta.get(), wq.get(), s);
+  }
   if (c->opt.self_term == 1) build_self_term(c, mesh, s);
   dV.release();
   dT.release();
   c->m2l_pairs_kp = 0;
-  if (!(c->opt.direct != 0 || c->tree.L < 2)) {
-    const int* tc = (c->nranks > 1) ? c->pan_own_cnt.get() : c->pan.cell_cnt.get();
+  if (!direct) {
+    const int* tc = (R > 1) ? c->pan_own_cnt.get() : c->pan.cell_cnt.get();
     if (rot_supported(c->P) && c->m2l_mode == 0) c->m2l_pairs_kp = m2l_work(c, src.cell_cnt.get(), tc, s).pairs;
     else c->m2l_pairs_kp = c->tree.m2l_pairs;
   }
@@ -705,6 +745,7 @@ void fmmbem_destroy(fmmbem_ctx* c) {
     }
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->join) cudaEventDestroy(c->join);
+    if (c->done) cudaEventDestroy(c->done);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -741,7 +782,9 @@ fmmbem_status fmmbem_matvec(fmmbem_ctx* c, fmmbem_op op, const float* x, float* 
   if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_A) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
   DevGuard dg(c->device);
   cudaStream_t st = (cudaStream_t)stream;
+  order_after_last(c, st);
   apply_op(c, op, x, y, st, true);
+  mark_done(c, st);
   return FMMBEM_OK;
   API_END
 }
@@ -832,6 +875,7 @@ fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, f
   if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_A) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
   DevGuard dg(c->device);
   cudaStream_t st = c->stream;
+  order_after_last(c, st);
   const int64_t n = c->n_own();
   c->tmp_x.alloc(std::max<int64_t>(n, 1));
   c->tmp_y.alloc(std::max<int64_t>(n, 1));
@@ -839,11 +883,13 @@ fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, f
                          c->tree.L >= 2 && std::getenv("FMMBEM_E2E_PLAIN") == nullptr;
   if (pipelined) {
     matvec_host_pipelined(c, op, xh, yh);
+    mark_done(c, st);
     return FMMBEM_OK;
   }
   FMM_CUDA(cudaMemcpyAsync(c->tmp_x.get(), xh, n * sizeof(float), cudaMemcpyHostToDevice, st));
   apply_op(c, op, c->tmp_x.get(), c->tmp_y.get(), st, true);
   FMM_CUDA(cudaMemcpyAsync(yh, c->tmp_y.get(), n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  mark_done(c, st);
   FMM_CUDA(cudaStreamSynchronize(st));
   return FMMBEM_OK;
   API_END
@@ -853,13 +899,21 @@ fmmbem_status fmmbem_charge_fields(fmmbem_ctx* c, float* En, float* psi) {
   API_BEGIN
   if (!c) throw Error(FMMBEM_E_INVALID, "null ctx");
   DevGuard dg(c->device);
+  order_after_last(c, c->stream);
   ensure_fields(c, c->stream);
   const size_t nb = c->n_own() * sizeof(float);
   if (En) FMM_CUDA(cudaMemcpyAsync(En, c->En.get(), nb, cudaMemcpyDeviceToDevice, c->stream));
   if (psi) FMM_CUDA(cudaMemcpyAsync(psi, c->psi.get(), nb, cudaMemcpyDeviceToDevice, c->stream));
+  mark_done(c, c->stream);
   FMM_CUDA(cudaStreamSynchronize(c->stream));
   return FMMBEM_OK;
   API_END
+}
+
+fmmbem_status fmmbem_reset_fields(fmmbem_ctx* c) {
+  if (!c) return FMMBEM_E_INVALID;
+  c->have_fields = false;
+  return FMMBEM_OK;
 }
 
 fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* c, fmmbem_bibee v, float* sig, fmmbem_energy* out) {
@@ -868,6 +922,8 @@ fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* c, fmmbem_bibee v, float* sig, fmm
   if (v < FMMBEM_BIBEE_CFA || v > FMMBEM_BIBEE_LB) throw Error(FMMBEM_E_INVALID, "bad BIBEE variant");
   DevGuard dg(c->device);
   cudaStream_t st = c->stream;
+  order_after_last(c, st);
+  FMM_CUDA(cudaEventRecord(c->ev[E_BIB0], st));
   ensure_fields(c, st);
   const double s = (v == FMMBEM_BIBEE_CFA) ? -0.5 : (v == FMMBEM_BIBEE_P ? 0.0 : 0.5);
   const double d = 1.0 - c->f * s;
@@ -883,6 +939,14 @@ fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* c, fmmbem_bibee v, float* sig, fmm
   if (n > 0) k_scale<<<ceil_div(n, 256), 256, 0, st>>>(sh, c->En.get(), n, (float)(c->f / d));
   FMM_CHECK_LAUNCH();
   const double e = 0.5 * dot_weighted(c, n, sh, c->psi.get(), c->pan.pos.get() + c->pan_lo, st);  // A20
+  FMM_CUDA(cudaEventRecord(c->ev[E_BIB1], st));
+  mark_done(c, st);
+  {
+    float ms = 0.f;
+    FMM_CUDA(cudaEventSynchronize(c->ev[E_BIB1]));
+    FMM_CUDA(cudaEventElapsedTime(&ms, c->ev[E_BIB0], c->ev[E_BIB1]));
+    c->last.bibee = ms;
+  }
   out->dG_internal = e;
   out->dG_kcal_mol = e * KCAL;
   out->iterations = 0;
@@ -901,6 +965,7 @@ fmmbem_status fmmbem_solve(fmmbem_ctx* c, const fmmbem_solve_options* so, float*
     throw Error(FMMBEM_E_INVALID, "bad solve options");
   DevGuard dg(c->device);
   cudaStream_t st = c->stream;
+  order_after_last(c, st);
   ensure_fields(c, st);
   if (c->red.n < (size_t)o.restart + 2) c->red.alloc(o.restart + 2 + 64);
   DevBuf<float> b, xs;
@@ -924,6 +989,7 @@ fmmbem_status fmmbem_solve(fmmbem_ctx* c, const fmmbem_solve_options* so, float*
   fmmbem_status stt = gmres_solve(c, b.get(), x, o.tol, o.restart, o.max_iters, o.x0_dev, hist, &its, &rr, st);
   cudaEventRecord(e1, st);
   const double e = 0.5 * dot_weighted(c, n, x, c->psi.get(), c->pan.pos.get() + c->pan_lo, st);
+  mark_done(c, st);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -943,27 +1009,41 @@ fmmbem_status fmmbem_reaction_potential(fmmbem_ctx* c, const float* sigma, doubl
   if (c->nc == 0) return FMMBEM_OK;
   DevGuard dg(c->device);
   cudaStream_t st = c->stream;
+  order_after_last(c, st);
   DevBuf<float> y;
   DevBuf<double> yd;
   y.alloc(c->nc);
   yd.alloc(c->nc);
-  TgtArg t;  // every charge, on every rank (diagnostic path, replicated after the all-gather)
+  y.zero(st);
+  yd.zero(st);
+  // targets: the charges of this rank's leaves (every charge with one rank); sources: the panels
+  // (owned + halo weights, the LET multipoles of the other ranks' panels)
+  TgtArg t;
   t.set = &c->chg;
+  bool dist = false;
+  SrcArg s = kp_src(c, sigma, st, &dist);
+  int64_t c0 = 0, c1 = c->nc;
+  if (multi(c)) {
+    t.leaf_lo = c->leaf_lo;
+    t.leaf_hi = c->leaf_hi;
+    t.cnt = c->chg_own_cnt.get();
+    int h[2];
+    FMM_CUDA(cudaMemcpyAsync(&h[0], c->chg.begin.get() + c->leaf_lo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaMemcpyAsync(&h[1], c->chg.begin.get() + c->leaf_hi, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    c0 = h[0];
+    c1 = h[1];
+  }
   Outputs o;
   o.pot.y = y.get();
   o.pot.b = (float)(1.0 / FOUR_PI);
-  SrcArg s;
-  s.set = (c->K == 1) ? &c->pan : &c->quad;
-  s.x = sigma;
-  if (c->nranks > 1) {
-    c->xfull.alloc(c->np);
-    comm_allgatherv_f32(c, sigma, c->xfull.get(), c->pan_offs, st);
-    s.x = c->xfull.get();
-  }
-  fmm_eval(c, t, s, o, false, false, st, false, false);
-  k_unpermute<<<ceil_div(c->nc, 256), 256, 0, st>>>(c->nc, c->chg_ids.get(), y.get(), yd.get());
+  fmm_eval(c, t, s, o, false, false, st, false, dist);
+  if (c1 > c0)
+    k_unpermute<<<ceil_div(c1 - c0, 256), 256, 0, st>>>(c1 - c0, c->chg_ids.get() + c0, y.get() + c0, yd.get());
   FMM_CHECK_LAUNCH();
+  comm_allreduce_f64(c, yd.get(), c->nc, st);  // every charge written by exactly one rank
   FMM_CUDA(cudaMemcpyAsync(phi, yd.get(), c->nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  mark_done(c, st);
   FMM_CUDA(cudaStreamSynchronize(st));
   return FMMBEM_OK;
   API_END

@@ -28,6 +28,7 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
@@ -54,6 +55,7 @@ NcclApi& api() {
   a.commSplit = (decltype(a.commSplit))dlsym(a.h, "ncclCommSplit");
   a.allReduce = (decltype(a.allReduce))sym("ncclAllReduce");
   a.broadcast = (decltype(a.broadcast))sym("ncclBroadcast");
+  a.allGather = (decltype(a.allGather))sym("ncclAllGather");
   a.send = (decltype(a.send))sym("ncclSend");
   a.recv = (decltype(a.recv))sym("ncclRecv");
   a.groupStart = (decltype(a.groupStart))sym("ncclGroupStart");
@@ -129,6 +131,51 @@ void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std
     if (p == c->opt.rank) continue;
     if (scnt[p]) check(api().send(sbuf[p], scnt[p], ncclFloat32, p, (ncclComm_t)c->comm, s), "ncclSend");
     if (rcnt[p]) check(api().recv(rbuf[p], rcnt[p], ncclFloat32, p, (ncclComm_t)c->comm, s), "ncclRecv");
+  }
+  check(api().groupEnd(), "ncclGroupEnd");
+}
+
+// element-wise min / max of n doubles over ranks (device buffer, in place)
+void comm_allreduce_f64_op(fmmbem_ctx* c, double* buf, size_t n, int op, cudaStream_t s) {
+  if (c->opt.nranks <= 1 || n == 0) return;
+  const ncclRedOp_t o = op < 0 ? ncclMin : (op > 0 ? ncclMax : ncclSum);
+  check(api().allReduce(buf, buf, n, ncclFloat64, o, (ncclComm_t)c->comm, s), "ncclAllReduce");
+}
+
+// every rank's `n` int64 values (device) -> all[r * n + k] (device)
+void comm_allgather_i64(fmmbem_ctx* c, const int64_t* mine, int64_t* all, size_t n, cudaStream_t s) {
+  check(api().allGather(mine, all, n, ncclInt64, (ncclComm_t)c->comm, s), "ncclAllGather");
+}
+
+// uneven all-gather of raw bytes: full[offs[r] : offs[r+1]] <- rank r's `mine` (grouped broadcasts)
+void comm_allgatherv_bytes(fmmbem_ctx* c, const void* mine, void* full, const std::vector<size_t>& offs,
+                           cudaStream_t s) {
+  const int R = c->opt.nranks;
+  char* f = static_cast<char*>(full);
+  check(api().groupStart(), "ncclGroupStart");
+  for (int r = 0; r < R; ++r) {
+    const size_t n = offs[r + 1] - offs[r];
+    if (!n) continue;
+    check(api().broadcast(r == c->opt.rank ? mine : (const void*)(f + offs[r]), f + offs[r], n, ncclUint8, r,
+                          (ncclComm_t)c->comm, s),
+          "ncclBroadcast");
+  }
+  check(api().groupEnd(), "ncclGroupEnd");
+}
+
+// grouped point-to-point exchange of raw bytes (any peer may be this rank: local device copy)
+void comm_alltoallv_bytes(fmmbem_ctx* c, const std::vector<const void*>& sbuf, const std::vector<size_t>& sbytes,
+                          const std::vector<void*>& rbuf, const std::vector<size_t>& rbytes, cudaStream_t s,
+                          bool second) {
+  const int R = c->opt.nranks, me = c->opt.rank;
+  const ncclComm_t cm = (ncclComm_t)(second && c->comm2 ? c->comm2 : c->comm);
+  if (sbytes[me]) FMM_CUDA(cudaMemcpyAsync(rbuf[me], sbuf[me], sbytes[me], cudaMemcpyDeviceToDevice, s));
+  if (R <= 1) return;
+  check(api().groupStart(), "ncclGroupStart");
+  for (int p = 0; p < R; ++p) {
+    if (p == me) continue;
+    if (sbytes[p]) check(api().send(sbuf[p], sbytes[p], ncclUint8, p, cm, s), "ncclSend");
+    if (rbytes[p]) check(api().recv(rbuf[p], rbytes[p], ncclUint8, p, cm, s), "ncclRecv");
   }
   check(api().groupEnd(), "ncclGroupEnd");
 }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "plan.h"
 
 namespace fmm {
 
@@ -73,9 +74,25 @@ struct LetPlan {
   int64_t cells_sent = 0, cells_recv = 0;
 };
 
-struct Timing {
-  cudaEvent_t ev[12];
-  bool valid = false;
+// panels of this rank's input slice (device, FP64, in the caller's order of the slice)
+struct PanelInput {
+  int64_t n = 0;     // panels in the slice
+  int64_t gid0 = 0;  // global id (caller triangle index) of the slice's first panel
+  const double* cen = nullptr;
+  const double* nrm = nullptr;
+  const double* area = nullptr;
+  const double* qp = nullptr;  // K > 1: quadrature points [n][K][3]
+};
+
+// near-field halo (multi-GPU, SURVEY 8(e) "halo source weights"): the owned panels every peer's
+// P2P needs (their leaves neighbour a leaf of the peer) and the peers' panels this rank's P2P needs.
+// Local point arrays are [halo of lower ranks | owned | halo of higher ranks], in leaf order.
+struct HaloPlan {
+  std::vector<int64_t> scnt, soff;  // per peer: panels sent, first entry in sidx
+  std::vector<int64_t> rcnt, roff;  // per peer: panels received, first local index of the segment
+  DevBuf<int> sidx;                 // owned-relative index of every panel sent (peers concatenated)
+  DevBuf<float> sbuf;               // packed x of one matvec
+  int64_t sent = 0, recv = 0;
 };
 
 }  // namespace fmm
@@ -84,7 +101,7 @@ struct fmmbem_ctx {
   fmmbem_options opt{};
   int P = 10, K = 1, NC = 55;  // terms, quadrature points, complex coefficients per expansion
   double eps_in = 4, eps_out = 80, f = 0, eps_hat = 0;
-  int64_t np = 0, nc = 0;
+  int64_t np = 0, nc = 0;  // panels of ALL ranks, charges (replicated)
   int device = 0;
   cudaStream_t stream = nullptr;  // internal stream for setup / host-buffer calls
 
@@ -118,30 +135,34 @@ struct fmmbem_ctx {
   int m2l_mode = 0;  // 0 = rotation O(P^3) when available, 1 = plain O(P^4)
   int p2p_chunk = 64;   // P2P targets per work item (FMMBEM_P2P_CHUNK)
   fmm::DevBuf<float4> p2p_src;  // scaled-form P2P sources of the current matvec (a y, a)
+  fmm::DevBuf<unsigned> p2p_wmax;  // bits of max |w| the table was normalised by (power of two, P2P epilogue)
   int p2p_occ = 1;      // scaled K' P2P at 32 resident warps per SM (<= 64 registers; FMMBEM_P2P_OCC=0 -> 72)
   int p2p_scaled = 1;   // scaled-coordinate K' P2P (FMMBEM_P2P_PLAIN=1 -> plain form)
-  int64_t p2p_inter_kp = 0, p2p_inter_chg = 0;  // exact interaction counts
+  int64_t p2p_inter_kp = 0;  // exact P2P interaction count of the K' / A matvec
   int64_t m2l_pairs_kp = 0;
-  // multi-GPU partition: this rank owns leaves [leaf_lo, leaf_hi) and the panels
-  // [pan_lo, pan_hi) of the tree order; pan_offs[r] = first panel of rank r
+  // multi-GPU partition: this rank owns leaves [leaf_lo, leaf_hi); its panels are the
+  // local points [pan_lo, pan_hi) of pan (the rest of pan is the near-field halo)
   void* comm = nullptr;   // ncclComm_t (nranks > 1)
-  void* comm2 = nullptr;  // second communicator (ncclCommSplit) for the x all-gather, so it can run
+  void* comm2 = nullptr;  // second communicator (ncclCommSplit) for the halo exchange, so it can run
                           // on the caller's stream concurrently with the multipole exchange
   int rank = 0, nranks = 1;
   int leaf_lo = 0, leaf_hi = 0;
   int64_t pan_lo = 0, pan_hi = 0;
-  std::vector<int64_t> pan_offs;
-  fmm::DevBuf<int> pan_own_cnt, quad_own_cnt;  // subtree counts of owned points
-  fmm::DevBuf<float> xfull;                    // all-gathered source weights
+  fmm::DevBuf<int> pan_own_cnt, quad_own_cnt, chg_own_cnt;  // subtree counts of owned points
   fmm::DevBuf<float> selfd;                    // [np] curvature self-term K'_ii in local order (self_term = 1)
   fmm::NearCSR near;                           // near_mode = 1 corrections
   fmm::LetPlan let;                            // multipole LET exchange plan (nranks > 1)
   std::vector<int64_t> leaf_bounds;            // [nranks + 1] leaf partition
+  fmm::DevBuf<int> gbeg;                       // [n_leaves + 1] GLOBAL panel CSR over leaves (all ranks)
+  fmm::HaloPlan halo;                          // near-field halo exchange (nranks > 1)
+  fmm::ExchangePlan xplan;                     // host plan: partition, halo leaves, LET cells (plan.cu)
+  fmm::DevBuf<float> xext;                     // [pan.n] source weights incl. the halo (nranks > 1)
   int64_t n_own() const { return pan_hi - pan_lo; }
   fmmbem_timing last{};
   // phase events (E_* in api.cu); recorded on the stream that runs the phase
-  cudaEvent_t ev[20] = {};
+  cudaEvent_t ev[24] = {};
   cudaEvent_t fork = nullptr, join = nullptr;  // untimed fork/join of the far-field stream
+  cudaEvent_t done = nullptr;  // end of the last stream-ordered call (every entry point waits on it first)
   cudaStream_t side = nullptr;                 // far-field chain runs here when overlap is on
   int overlap = 0;                             // 1: P2P concurrent with the upward/M2L/exchange chain
   bool timed_xg = false;

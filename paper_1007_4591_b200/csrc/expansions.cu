@@ -55,27 +55,34 @@ __device__ __forceinline__ void column_acc(float2 (&a)[P - m], float4 u, float r
 
 // columns m and P-1-m together (P+1 coefficients, two independent recurrences per source); the
 // lanes' partial sums are transposed through red[P+1][33] and lane c (< P+1) adds the 32 partials of
-// entry c to its register accumulator acc[m] (fixed order, no atomics)
+// entry c to its register accumulator acc[m] (fixed order, no atomics).  Odd P: the middle column
+// m = (P-1)/2 is reduced alone (P - m coefficients).
 template <int P, int m>
-__device__ __forceinline__ void p2m_columns(float2 (&acc)[P / 2], float2* red, const float4* src, int ns, int lane) {
+__device__ __forceinline__ void p2m_columns(float2 (&acc)[(P + 1) / 2], float2* red, const float4* src, int ns,
+                                            int lane) {
   constexpr int m2 = P - 1 - m;
-  float2 a[P - m], b[P - m2];
+  constexpr bool single = (m == m2);
+  constexpr int NB = single ? 1 : P - m2;
+  float2 a[P - m], b[NB];
 #pragma unroll
   for (int k = 0; k < P - m; ++k) a[k] = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int k = 0; k < P - m2; ++k) b[k] = make_float2(0.f, 0.f);
+  for (int k = 0; k < NB; ++k) b[k] = make_float2(0.f, 0.f);
   for (int j = lane; j < ns; j += 32) {
     const float4 u = src[j];
     const float r2 = fmaf(u.x, u.x, fmaf(u.y, u.y, u.z * u.z));
     column_acc<P, m>(a, u, r2);
-    column_acc<P, m2>(b, u, r2);
+    if constexpr (!single) column_acc<P, m2>(b, u, r2);
   }
 #pragma unroll
   for (int k = 0; k < P - m; ++k) red[k * 33 + lane] = a[k];
+  if constexpr (!single) {
 #pragma unroll
-  for (int k = 0; k < P - m2; ++k) red[(P - m + k) * 33 + lane] = b[k];
+    for (int k = 0; k < P - m2; ++k) red[(P - m + k) * 33 + lane] = b[k];
+  }
   __syncwarp();
-  if (lane < P + 1) {
+  constexpr int NE = single ? P - m : P + 1;
+  if (lane < NE) {
     float2 s0 = make_float2(0.f, 0.f), s1 = s0;
 #pragma unroll
     for (int l = 0; l < 32; l += 2) {
@@ -85,7 +92,7 @@ __device__ __forceinline__ void p2m_columns(float2 (&acc)[P / 2], float2* red, c
     acc[m] = __fadd2_rn(acc[m], __fadd2_rn(s0, s1));
   }
   __syncwarp();
-  if constexpr (m + 1 < m2) p2m_columns<P, m + 1>(acc, red, src, ns, lane);
+  if constexpr (m + 1 <= P - 2 - m) p2m_columns<P, m + 1>(acc, red, src, ns, lane);
 }
 
 // P2M, one warp per leaf: the leaf's sources are scaled into the cell frame and staged in shared
@@ -96,17 +103,17 @@ template <int P>
 __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
                                               const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               float2* __restrict__ M) {
-  static_assert(P % 2 == 0, "column pairs");
   constexpr int NC = P * (P + 1) / 2;
+  constexpr int NPAIR = (P + 1) / 2;  // column pairs (m, P-1-m); odd P: the last one is the middle column
   __shared__ float2 red[(P + 1) * 33];
   __shared__ float4 src[P2M_TILE];
   const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
-  float2 acc[P / 2];
+  float2 acc[NPAIR];
 #pragma unroll
-  for (int k = 0; k < P / 2; ++k) acc[k] = make_float2(0.f, 0.f);
+  for (int k = 0; k < NPAIR; ++k) acc[k] = make_float2(0.f, 0.f);
   for (int t0 = b; t0 < e; t0 += P2M_TILE) {
     const int ns = min(P2M_TILE, e - t0);
     __syncwarp();
@@ -123,9 +130,10 @@ __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, co
   if (lane < P + 1) {
     float2* Mo = M + (size_t)(leaf_off + leaf) * NC;
 #pragma unroll
-    for (int m = 0; m < P / 2; ++m) {
+    for (int m = 0; m < NPAIR; ++m) {
       const int m2 = P - 1 - m;
       // entry lane: (n = m + lane, m) for lane < P - m, else (n = m2 + lane - (P - m), m2)
+      if (m == m2 && lane >= P - m) continue;  // odd P: the middle column has P - m entries
       const int n = lane < P - m ? m + lane : m2 + lane - (P - m);
       const int mm = lane < P - m ? m : m2;
       Mo[cx(n, mm)] = acc[m];
@@ -238,7 +246,7 @@ void l2p_dispatch(int grid, const float4* pos, const float4* nrm, const int* beg
 
 }  // namespace
 
-bool exp_specialised(int P) { return P == 8 || P == 10 || P == 12 || P == 14; }
+bool exp_specialised(int P) { return P == 8 || P == 10 || P == 12 || P == 13 || P == 14; }
 
 void launch_p2m_t(int P, int grid, const float4* pos, const float* x, int div, const int* beg, float inv_w,
                   int leaf_off, int leaf0, float2* M, cudaStream_t st) {
@@ -247,6 +255,7 @@ void launch_p2m_t(int P, int grid, const float4* pos, const float* x, int div, c
     case 8: k_p2m_t<8><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
     case 10: k_p2m_t<10><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
     case 12: k_p2m_t<12><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
+    case 13: k_p2m_t<13><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
     case 14: k_p2m_t<14><<<grid, 32, 0, st>>>(pos, x, div, beg, inv_w, leaf_off, leaf0, M); break;
     default: throw Error(FMMBEM_E_INVALID, "P2M not specialised for this P");
   }
@@ -260,6 +269,7 @@ void launch_l2p_t(int P, int grid, const float4* pos, const float4* nrm, const i
     case 8: l2p_dispatch<8>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
     case 10: l2p_dispatch<10>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
     case 12: l2p_dispatch<12>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
+    case 13: l2p_dispatch<13>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
     case 14: l2p_dispatch<14>(grid, pos, nrm, beg, inv_w, leaf_off, leaf0, Lx, pot, dn, st); break;
     default: throw Error(FMMBEM_E_INVALID, "L2P not specialised for this P");
   }

@@ -22,8 +22,9 @@
 //        dz R_j^k = R_{j-1}^k,  dx R_j^k = (R_{j-1}^{k+1} - R_{j-1}^{k-1})/2,
 //        dy R_j^k = -i (R_{j-1}^{k+1} + R_{j-1}^{k-1})/2
 // Storage: m >= 0 only, index n(n+1)/2 + m, float2 (re, im); negative orders follow from
-// X_n^{-m} = (-1)^m conj(X_n^m).  The M2L is the plain O(P^4) translation in this round
-// (rotation-accelerated O(P^3), is the next step).
+// X_n^{-m} = (-1)^m conj(X_n^m).  The kernels here are the generic O(P^4) translations, kept as
+// the independent cross-check of the rotation-accelerated O(P^3) M2M / M2L / L2L of m2l_rot.cu
+// that run by default, and as the fallback for orders without a rotation instantiation.
 #include <cmath>
 #include <complex>
 

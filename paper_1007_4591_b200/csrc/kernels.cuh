@@ -23,8 +23,7 @@ struct OutArg {
 struct SrcArg {
   const PointSet* set = nullptr;
   const float* x = nullptr;
-  const float* x_far = nullptr;  // weights for the upward sweep if different from x (owned slice view)
-  const float* ag_src = nullptr;  // deferred all-gather ag_src -> x (run by fmm_eval before P2P)
+  const float* halo_src = nullptr;  // nranks > 1: owned weights whose halo exchange fmm_eval runs before P2P
   const float4* scaled = nullptr;  // prepared scaled-form P2P sources (prepare_p2p_sources), else built in launch_p2p
   int leaf_lo = 0, leaf_hi = -1;
   const int* cnt = nullptr;
@@ -42,8 +41,11 @@ struct Outputs {
   OutArg dn;   // normal derivative n . grad phi             (raw, before b)
 };
 
-void build_tree(fmmbem_ctx* c, const double* cen, const double* nrm, const double* area, const double* qpts,
-                const double* wq, const double* cxyz, const double* cq, cudaStream_t s);
+void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const double* cxyz, const double* cq,
+                cudaStream_t s);
+// per-matvec near-field halo (nranks > 1): owned x into c->xext, then the peers' halo weights
+void halo_copy_owned(fmmbem_ctx* c, const float* x_owned, cudaStream_t st);
+void halo_exchange(fmmbem_ctx* c, const float* x_owned, cudaStream_t st);
 
 // near field; writes y = ax x + b raw (overwrites)
 // per-matvec scaled-form source table (a y, a) of the K' / A near field into c->p2p_src
@@ -66,6 +68,13 @@ void comm_allreduce_f64(fmmbem_ctx* c, double* buf, size_t n, cudaStream_t s);
 void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const std::vector<int64_t>& offs,
                          cudaStream_t s, bool second = false);
 void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds);
+void comm_allreduce_f64_op(fmmbem_ctx* c, double* buf, size_t n, int op /* -1 min, 0 sum, +1 max */, cudaStream_t s);
+void comm_allgather_i64(fmmbem_ctx* c, const int64_t* mine, int64_t* all, size_t n, cudaStream_t s);
+void comm_allgatherv_bytes(fmmbem_ctx* c, const void* mine, void* full, const std::vector<size_t>& offs,
+                           cudaStream_t s);
+void comm_alltoallv_bytes(fmmbem_ctx* c, const std::vector<const void*>& sbuf, const std::vector<size_t>& sbytes,
+                          const std::vector<void*>& rbuf, const std::vector<size_t>& rbytes, cudaStream_t s,
+                          bool second = false);
 void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std::vector<size_t>& scnt,
                        const std::vector<float*>& rbuf, const std::vector<size_t>& rcnt, cudaStream_t s);
 void build_let(fmmbem_ctx* c, const std::vector<int64_t>& leaf_bounds, cudaStream_t s);

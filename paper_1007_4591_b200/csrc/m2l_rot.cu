@@ -48,7 +48,7 @@ __host__ __device__ constexpr int boff(int n) {  // sum_{k<n} pad4((k+1)^2)
   for (int k = 0; k < n; ++k) o += pad4((k + 1) * (k + 1));
   return o;
 }
-constexpr int RMAXC = 12;  // highest instantiated rotation order
+constexpr int RMAXC = 14;  // highest instantiated rotation order
 constexpr int TSZ = boff(RMAXC);
 struct RotTab {
   float v[4][TSZ];
@@ -58,21 +58,40 @@ __host__ __device__ constexpr double cfact(int n) {
   for (int i = 2; i <= n; ++i) f *= (double)i;
   return f;
 }
-__host__ __device__ constexpr double w_half_pi(int n, int mp, int m, int sgn) {  // W^n_{mp,m}(sgn pi/2)
-  double t = 0.0;
-  const int k0 = (m - mp) > 0 ? (m - mp) : 0, k1 = (n + m) < (n - mp) ? (n + m) : (n - mp);
-  for (int k = k0; k <= k1; ++k)
-    t += (((mp - m + k) & 1) ? -1.0 : 1.0) / (cfact(n + m - k) * cfact(k) * cfact(mp - m + k) * cfact(n - mp - k));
-  double sc = cfact(n + m) * cfact(n - m);
-  for (int i = 0; i < n; ++i) sc *= 0.5;
-  if (sgn < 0 && ((mp - m) & 1)) sc = -sc;
-  return t * sc;
+// W^n_{mp,m}(+pi/2) for |mp|, |m| <= n < RMAXC, from a factorial table (keeps the constant
+// evaluation within the compiler's step budget); W(-pi/2) = (-1)^(mp-m) W(+pi/2)
+struct WTab {
+  double fact[2 * RMAXC + 1];
+  double v[RMAXC][2 * RMAXC - 1][2 * RMAXC - 1];
+};
+__host__ __device__ constexpr WTab make_w() {
+  WTab t{};
+  t.fact[0] = 1.0;
+  for (int i = 1; i <= 2 * RMAXC; ++i) t.fact[i] = t.fact[i - 1] * (double)i;
+  for (int n = 0; n < RMAXC; ++n)
+    for (int mp = -n; mp <= n; ++mp)
+      for (int m = -n; m <= n; ++m) {
+        double s = 0.0;
+        const int k0 = (m - mp) > 0 ? (m - mp) : 0, k1 = (n + m) < (n - mp) ? (n + m) : (n - mp);
+        for (int k = k0; k <= k1; ++k)
+          s += (((mp - m + k) & 1) ? -1.0 : 1.0) /
+               (t.fact[n + m - k] * t.fact[k] * t.fact[mp - m + k] * t.fact[n - mp - k]);
+        double sc = t.fact[n + m] * t.fact[n - m];
+        for (int i = 0; i < n; ++i) sc *= 0.5;
+        t.v[n][mp + n][m + n] = s * sc;
+      }
+  return t;
 }
-__host__ __device__ constexpr double x_entry(int X, int n, int a, int b) {
-  return X == 0 ? w_half_pi(n, a, b, -1) : X == 1 ? w_half_pi(n, a, b, 1) : X == 2 ? w_half_pi(n, b, a, 1)
-                                                                               : w_half_pi(n, b, a, -1);
+__host__ __device__ constexpr double w_half_pi(const WTab& w, int n, int mp, int m, int sgn) {  // W^n_{mp,m}(sgn pi/2)
+  const double v = w.v[n][mp + n][m + n];
+  return (sgn < 0 && ((mp - m) & 1)) ? -v : v;
+}
+__host__ __device__ constexpr double x_entry(const WTab& w, int X, int n, int a, int b) {
+  return X == 0 ? w_half_pi(w, n, a, b, -1) : X == 1 ? w_half_pi(w, n, a, b, 1) : X == 2 ? w_half_pi(w, n, b, a, 1)
+                                                                                     : w_half_pi(w, n, b, a, -1);
 }
 __host__ __device__ constexpr RotTab make_rot() {
+  constexpr WTab w = make_w();
   RotTab t{};
   for (int X = 0; X < 4; ++X)
     for (int n = 0; n < RMAXC; ++n)
@@ -80,11 +99,11 @@ __host__ __device__ constexpr RotTab make_rot() {
         for (int m = 0; m <= n; ++m) {
           double v = 0.0;
           if (m == 0) {
-            if (((n + mp) & 1) == 0) v = x_entry(X, n, mp, 0);  // E_m'0 = X_m'0, F_m'0 = 0
+            if (((n + mp) & 1) == 0) v = x_entry(w, X, n, mp, 0);  // E_m'0 = X_m'0, F_m'0 = 0
           } else {
             const double sg = (m & 1) ? -1.0 : 1.0;
-            v = ((n + m + mp) & 1) == 0 ? x_entry(X, n, mp, m) + sg * x_entry(X, n, mp, -m)
-                                        : x_entry(X, n, mp, m) - sg * x_entry(X, n, mp, -m);
+            v = ((n + m + mp) & 1) == 0 ? x_entry(w, X, n, mp, m) + sg * x_entry(w, X, n, mp, -m)
+                                        : x_entry(w, X, n, mp, m) - sg * x_entry(w, X, n, mp, -m);
           }
           t.v[X][boff(n) + mp * (n + 1) + m] = (float)v;
         }
@@ -648,7 +667,7 @@ __global__ void k_row_flags(int n, const int* __restrict__ cnt, int* flag) {
 }  // namespace
 
 // instantiated orders (others use the O(P^4) kernel in farfield.cu)
-bool rot_supported(int P) { return P == 8 || P == 10 || P == 12; }
+bool rot_supported(int P) { return P == 8 || P == 10 || P == 12 || P == 13 || P == 14; }
 
 void init_rot_tables() {
   static bool done = false;
@@ -721,7 +740,7 @@ const M2LWork& m2l_work(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, c
   return *c->m2l_cache.back();
 }
 
-bool m2m_rot_supported(int P) { return P == 8 || P == 10 || P == 12; }
+bool m2m_rot_supported(int P) { return rot_supported(P); }
 
 // M2M of level l (children at l + 1); scratch T must hold n_cells * NC float2
 void launch_m2m_rot(fmmbem_ctx* c, int l, const int* scnt, float2* T, cudaStream_t st) {
@@ -732,6 +751,8 @@ void launch_m2m_rot(fmmbem_ctx* c, int l, const int* scnt, float2* T, cudaStream
     case 8: k_m2m_rot<8><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
     case 10: k_m2m_rot<10><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
     case 12: k_m2m_rot<12><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
+    case 13: k_m2m_rot<13><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
+    case 14: k_m2m_rot<14><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
     default: throw Error(FMMBEM_E_INVALID, "M2M rotation not instantiated for this P");
   }
   k_m2m_sum<<<ceil_div((int64_t)np * c->NC, 256), 256, 0, st>>>(p0, np, c->NC, Tr.child_begin.get(),
@@ -747,6 +768,8 @@ void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st) {
     case 8: k_l2l_rot<8><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
     case 10: k_l2l_rot<10><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
     case 12: k_l2l_rot<12><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
+    case 13: k_l2l_rot<13><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
+    case 14: k_l2l_rot<14><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
     default: throw Error(FMMBEM_E_INVALID, "L2L rotation not instantiated for this P");
   }
   FMM_CHECK_LAUNCH();
@@ -766,34 +789,30 @@ void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem
                                                                    c->Lx.get());
 }
 
+// lockstep warps per CTA: as many per-warp slots (NC x 33 float2) as fit the SM's 227 KB of shared
+// memory -- one CTA per SM (P = 12: 11 warps, 13: 9, 14: 8)
+constexpr int m2l_warps(int P) { return (227 * 1024) / ((P * (P + 1) / 2) * 33 * 8); }
+
 void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
   if (w.rows == 0) return;
   const Tree& T = c->tree;
-  // default: 11 lockstep warps per CTA (11 x 20.6 KB of slots at P = 12: one CTA fills the SM's
-  // shared memory); FMMBEM_M2L_WARPS = 1 / 2 selects the independent-warp kernel
-  static const int warps = [] {
+  // default: the lockstep kernel; FMMBEM_M2L_WARPS = 1 selects the independent-warp kernel (cross-check)
+  static const bool indep = [] {
     const char* e = std::getenv("FMMBEM_M2L_WARPS");
-    return e ? std::atoi(e) : 11;
+    return e && std::atoi(e) == 1;
   }();
-#define FMM_ROT_CASE(PP)                                                                                     \
-  case PP:                                                                                                   \
-    if (warps >= 3) {                                                                                        \
-      const size_t smem = (size_t)warps * (PP * (PP + 1) / 2) * 33 * sizeof(float2);                        \
-      switch (warps) {                                                                                       \
-        case 4: m2l_sync_launch<PP, 4>(w, T, c, smem, st); break;                                            \
-        case 8: m2l_sync_launch<PP, 8>(w, T, c, smem, st); break;                                            \
-        case 11: m2l_sync_launch<PP, 11>(w, T, c, smem, st); break;                                          \
-        default: m2l_sync_launch<PP, 10>(w, T, c, smem, st); break;                                          \
-      }                                                                                                      \
-    } else if (warps == 2)                                                                                   \
-      k_m2l_rot<PP, 2><<<ceil_div(w.rows, 2), 64, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(),          \
-                                                            w.idx.get(), T.key.get(), c->Mx.get(), c->Lx.get()); \
-    else                                                                                                     \
-      k_m2l_rot<PP, 1><<<(int)w.rows, 32, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(), w.idx.get(),     \
-                                                   T.key.get(), c->Mx.get(), c->Lx.get());                   \
+#define FMM_ROT_CASE(PP)                                                                                   \
+  case PP:                                                                                                 \
+    if (!indep) {                                                                                          \
+      constexpr int W = m2l_warps(PP);                                                                     \
+      m2l_sync_launch<PP, W>(w, T, c, (size_t)W * (PP * (PP + 1) / 2) * 33 * sizeof(float2), st);        \
+    } else {                                                                                               \
+      k_m2l_rot<PP, 1><<<(int)w.rows, 32, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(), w.idx.get(),   \
+                                                   T.key.get(), c->Mx.get(), c->Lx.get());                 \
+    }                                                                                                      \
     break;
   switch (c->P) {
-    FMM_ROT_CASE(8) FMM_ROT_CASE(10) FMM_ROT_CASE(12)
+    FMM_ROT_CASE(8) FMM_ROT_CASE(10) FMM_ROT_CASE(12) FMM_ROT_CASE(13) FMM_ROT_CASE(14)
     default: throw Error(FMMBEM_E_INVALID, "rotation M2L not instantiated for this P");
   }
 #undef FMM_ROT_CASE

@@ -44,6 +44,7 @@ struct P2PArgs {
   const int* tbeg;
   const float4* spos;
   const float4* ssc;  // scaled form: per-source (a s, a) prepared by k_scale_src (SC kernels only)
+  const unsigned* wmax;  // scaled form: bits of the max |weight| the table was normalised by (k_absmax)
   const float* sx;
   int sdiv;
   const int* sbeg;
@@ -59,6 +60,12 @@ struct P2PArgs {
 };
 
 __device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+
+// exponent e of the scaled-form weight normalisation: 2^e > max |w| (k_absmax / k_scale_src)
+__device__ __forceinline__ int wmax_exp(unsigned bits) {
+  const float m = __uint_as_float(bits);
+  return m > 0.f ? ilogbf(m) + 1 : 0;
+}
 
 // One source against the lane's two targets with packed FP32x2 arithmetic (FADD2/FMUL2/FFMA2 on
 // sm_100a; the scalar source coordinate is a broadcast operand): 12 packed instructions + 2 MUFU.RSQ
@@ -122,6 +129,8 @@ __global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
 
   const int4 it = a.items[blockIdx.x];
   const int leaf = it.x, tb = it.y, nt = it.z;
+  int wexp = 0;
+  if (SC) wexp = wmax_exp(*a.wmax);
   const int lane = threadIdx.x;
   const int4 tc = a.ijk[leaf];
 
@@ -327,7 +336,9 @@ P2P_UNROLL_LOOP(P2P_UNROLL)
       }
       if (DN) {
         const float4 n = a.tnrm[i];
-        float v = a.dn.b * fmaf(n.x, gx[q], fmaf(n.y, gy[q], n.z * gz[q]));
+        float g = fmaf(n.x, gx[q], fmaf(n.y, gy[q], n.z * gz[q]));
+        if (SC) g = ldexpf(g, wexp);  // undo the power-of-two normalisation of the weights
+        float v = a.dn.b * g;
         if (a.dn.x) v = fmaf(a.dn.d ? fmaf(a.dn.b, a.dn.d[i], a.dn.ax) : a.dn.ax, a.dn.x[i], v);
         if (a.dn.acc) v = __fadd_rn(v, a.dn.y[i]);
         a.dn.y[i] = v;
@@ -349,16 +360,35 @@ void dispatch(const P2PArgs& a, bool pot, bool dn, bool scaled, bool occ, int gr
   else k_p2p<P2P_T, false, true, SELF, CHECK><<<grid, 32, 0, st>>>(a);
 }
 
-// Scaled-form source table for one matvec: a = sign(w) |w|^(-1/2) with w = (A_j w_g) x_j, stored as
-// (a y, a) in leaf-local coordinates (see interact2s).  A zero weight becomes a source at 1e18 with
-// a = 1 (its r'^-3 flushes to zero); the shift a * (leaf offset) added in the fill keeps it there.
+// Scaled-form source table for one matvec: a = sign(w') |w'|^(-1/2) with w' = 2^-e (A_j w_g) x_j,
+// stored as (a y, a) in leaf-local coordinates (see interact2s).  2^e is the power of two at or
+// above max |w| (k_absmax), so |w'| <= 1 whatever the scale of x: r'^2 = r^2 / |w'| and
+// r'^-3 = |w'|^(3/2) r^-3 stay inside FP32 (with -ftz a weight below ~1e-25 max|w| contributes 0,
+// a relative change far below FP32 rounding of the sum); the P2P epilogue multiplies by 2^e.
+// A zero weight becomes a source at 1e18 with a = 1 (its r'^-3 flushes to zero); the shift
+// a * (leaf offset) added in the fill keeps it there.
+// bits of max_j |pos_j.w x_j / div| (non-negative floats order like their bit patterns)
+__global__ void k_absmax(int64_t n, const float4* __restrict__ spos, const float* __restrict__ sx, int sdiv,
+                         unsigned* out) {
+  float m = 0.f;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    float w = __ldg(&spos[j].w);
+    if (sx) w *= __ldg(sx + (sdiv == 1 ? j : j / sdiv));
+    m = fmaxf(m, fabsf(w));
+  }
+  for (int d = 16; d > 0; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
 __global__ void k_scale_src(int64_t n, const float4* __restrict__ spos, const float* __restrict__ sx, int sdiv,
-                            float4* __restrict__ out) {
+                            const unsigned* __restrict__ wmax, float4* __restrict__ out) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
+  const int e = wmax_exp(*wmax);
   const float4 p = __ldg(spos + j);
   float w = p.w;
   if (sx) w *= __ldg(sx + (sdiv == 1 ? j : j / sdiv));
+  w = ldexpf(w, -e);
   float4 r;
   if (w == 0.f) {
     r = make_float4(1e18f, 1e18f, 1e18f, 1.f);
@@ -437,8 +467,14 @@ const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int lea
 const float4* prepare_p2p_sources(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
   const int64_t n = s.set->n;
   if ((int64_t)c->p2p_src.n < n) c->p2p_src.alloc(n);
-  if (n > 0)
-    k_scale_src<<<ceil_div(n, 256), 256, 0, st>>>(n, s.set->pos.get(), s.x, s.set->div, c->p2p_src.get());
+  if (c->p2p_wmax.n < 1) c->p2p_wmax.alloc(1);
+  FMM_CUDA(cudaMemsetAsync(c->p2p_wmax.get(), 0, sizeof(unsigned), st));
+  if (n > 0) {
+    k_absmax<<<std::min<int64_t>(4 * 148, ceil_div(n, 256)), 256, 0, st>>>(n, s.set->pos.get(), s.x, s.set->div,
+                                                                          c->p2p_wmax.get());
+    k_scale_src<<<ceil_div(n, 256), 256, 0, st>>>(n, s.set->pos.get(), s.x, s.set->div, c->p2p_wmax.get(),
+                                                   c->p2p_src.get());
+  }
   FMM_CHECK_LAUNCH();
   return c->p2p_src.get();
 }
@@ -476,6 +512,7 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   if (sc) {
     a.ssc = s.scaled;
     if (!a.ssc) a.ssc = prepare_p2p_sources(c, s, st);
+    a.wmax = c->p2p_wmax.get();
   }
   if (self) {
     if (check) dispatch<true, true>(a, pot, dn, sc, c->p2p_occ != 0, grid, st);

@@ -1,0 +1,245 @@
+// plan.cu -- the multi-GPU exchange plan, host code.
+//
+// Given the replicated leaf skeleton (sorted leaf keys at level L with their panel / charge counts)
+// every rank derives the SAME plan, without any handshake:
+//   * the cost-weighted contiguous leaf partition ("equally distribute the Morton-indexed
+//     boxes", weighted by P2P + M2L work instead of counted);
+//   * the near-field halo: rank r sends peer p its leaves that neighbour a leaf of p (P2P of p
+//     needs their panels) and receives p's leaves that neighbour one of its own;
+//   * the local essential tree ("the data that needs to be communicated consists of ME
+//     coefficients of the cells in the interaction list, at every level"): a cell of level >= 2 is
+//     PURE (all its leaves on one rank, which computes its whole multipole) or SHARED (straddles a
+//     boundary: partial multipoles on several ranks, summed by one all-reduce); rank r sends p the
+//     pure cells it owns that are in the interaction list of a cell holding targets of p.
+// fmmbem_create copies its device skeleton to the host and calls plan_exchange; fmmbem_plan_create
+// (ABI, host only) builds the skeleton lists here first, so tests can check the plan on a CPU.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+
+namespace fmm {
+
+namespace {
+
+int lower_bound_key(const std::vector<uint64_t>& a, int64_t lo, int64_t hi, uint64_t v) {
+  return (int)(std::lower_bound(a.begin() + lo, a.begin() + hi, v) - a.begin());
+}
+
+}  // namespace
+
+// Host skeleton from sorted unique leaf keys (level L): the same definitions as tree.cu's kernels
+// (P:566): neighbours = same-level cells with max |d ijk| <= 1 (incl. self); interaction list =
+// children of the parent's neighbours that are not neighbours.
+void host_tree(const uint64_t* leaf_keys, int64_t nl, int L, HostTree& T) {
+  T.L = L;
+  std::vector<std::vector<uint64_t>> lvl(L + 1);
+  lvl[L].assign(leaf_keys, leaf_keys + nl);
+  for (int l = L - 1; l >= 0; --l) {
+    for (uint64_t k : lvl[l + 1])
+      if (lvl[l].empty() || lvl[l].back() != (k >> 3)) lvl[l].push_back(k >> 3);
+  }
+  T.lvl_off.assign(L + 2, 0);
+  for (int l = 0; l <= L; ++l) T.lvl_off[l + 1] = T.lvl_off[l] + (int64_t)lvl[l].size();
+  T.key.clear();
+  for (int l = 0; l <= L; ++l) T.key.insert(T.key.end(), lvl[l].begin(), lvl[l].end());
+  const int64_t nc = T.lvl_off[L + 1];
+  T.child_b.assign(nc, 0);
+  T.child_e.assign(nc, 0);
+  for (int l = 0; l < L; ++l)
+    for (int64_t i = T.lvl_off[l]; i < T.lvl_off[l + 1]; ++i) {
+      T.child_b[i] = lower_bound_key(T.key, T.lvl_off[l + 1], T.lvl_off[l + 2], T.key[i] << 3);
+      T.child_e[i] = lower_bound_key(T.key, T.lvl_off[l + 1], T.lvl_off[l + 2], (T.key[i] + 1) << 3);
+    }
+  auto find = [&](int l, int x, int y, int z) -> int {
+    const int lim = 1 << l;
+    if (x < 0 || y < 0 || z < 0 || x >= lim || y >= lim || z >= lim) return -1;
+    const uint64_t k = morton(x, y, z);
+    const int i = lower_bound_key(T.key, T.lvl_off[l], T.lvl_off[l + 1], k);
+    return (i < T.lvl_off[l + 1] && T.key[i] == k) ? i : -1;
+  };
+  // neighbour lists of the leaves (leaf indices)
+  T.nbr_off.assign(nl + 1, 0);
+  T.nbr_idx.clear();
+  for (int64_t k = 0; k < nl; ++k) {
+    int x, y, z;
+    demorton(T.key[T.lvl_off[L] + k], x, y, z);
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int j = find(L, x + dx, y + dy, z + dz);
+          if (j >= 0) T.nbr_idx.push_back(j - (int)T.lvl_off[L]);
+        }
+    T.nbr_off[k + 1] = (int)T.nbr_idx.size();
+  }
+  // interaction lists of every cell of levels >= 2 (global cell indices)
+  T.m2l_off.assign(nc + 1, 0);
+  T.m2l_idx.clear();
+  for (int64_t c = 0; c < nc; ++c) {
+    int l = 0;
+    while (c >= T.lvl_off[l + 1]) ++l;
+    if (l >= 2) {
+      int x, y, z;
+      demorton(T.key[c], x, y, z);
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int p = find(l - 1, (x >> 1) + dx, (y >> 1) + dy, (z >> 1) + dz);
+            if (p < 0) continue;
+            for (int ch = T.child_b[p]; ch < T.child_e[p]; ++ch) {
+              int cx, cy, cz;
+              demorton(T.key[ch], cx, cy, cz);
+              if (std::abs(cx - x) <= 1 && std::abs(cy - y) <= 1 && std::abs(cz - z) <= 1) continue;
+              T.m2l_idx.push_back(ch);
+            }
+          }
+    }
+    T.m2l_off[c + 1] = (int)T.m2l_idx.size();
+  }
+}
+
+// Partition + halo + LET (see the file header).  leaf_pan / leaf_tgt: panels / target points
+// (panels + charges) per leaf of all ranks; K: quadrature points per panel (P2P sources).
+void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int K,
+                   int R, int me, ExchangePlan& X) {
+  const int L = T.L;
+  const int64_t nl = T.lvl_off[L + 1] - T.lvl_off[L], nc = T.lvl_off[L + 1];
+  const int64_t leaf0 = T.lvl_off[L];
+  // leaf cost: P2P interactions + M2L translations (~600 interaction-equivalents each) + per point
+  std::vector<double> cost(nl);
+  for (int64_t k = 0; k < nl; ++k) {
+    long long s = 0;
+    for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1]; ++e) s += leaf_pan[T.nbr_idx[e]];
+    const long long nt = leaf_pan[k];
+    const double m2l = (double)(T.m2l_off[leaf0 + k + 1] - T.m2l_off[leaf0 + k]);
+    cost[k] = (double)(nt * s * K) + (nt ? 600.0 * m2l : 0.0) + 50.0 * (double)nt;
+  }
+  X.leaf_bounds.assign(R + 1, 0);
+  split_costs(cost.data(), nl, R, X.leaf_bounds.data());
+  std::vector<int> lrank(nl);
+  for (int r = 0; r < R; ++r)
+    for (int64_t k = X.leaf_bounds[r]; k < X.leaf_bounds[r + 1]; ++k) lrank[k] = r;
+  const int lo = (int)X.leaf_bounds[me], hi = (int)X.leaf_bounds[me + 1];
+  // near-field halo
+  X.halo_send.assign(R, {});
+  X.halo_recv.assign(R, {});
+  for (int64_t k = 0; k < nl; ++k) {
+    if (lrank[k] == me) {
+      unsigned long long m = 0;
+      for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1]; ++e) m |= 1ULL << lrank[T.nbr_idx[e]];
+      for (int p = 0; p < R; ++p)
+        if (p != me && (m >> p & 1ULL)) X.halo_send[p].push_back((int)k);
+    } else {
+      bool need = false;
+      for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1] && !need; ++e) need = lrank[T.nbr_idx[e]] == me;
+      if (need) X.halo_recv[lrank[k]].push_back((int)k);
+    }
+  }
+  (void)lo;
+  (void)hi;
+  // local essential tree: leaf range and owner of every cell (levels >= 2), sources per cell
+  std::vector<long long> tpre(nl + 1, 0), ppre(nl + 1, 0);
+  for (int64_t k = 0; k < nl; ++k) {
+    tpre[k + 1] = tpre[k] + leaf_tgt[k];
+    ppre[k + 1] = ppre[k] + leaf_pan[k];
+  }
+  const int64_t c0 = T.lvl_off[std::min(2, L + 1)];
+  std::vector<int> first(nc, 0), end(nc, 0), owner(nc, -1);
+  std::vector<char> has_src(nc, 0);
+  for (int64_t c = c0; c < nc; ++c) {
+    int l = 0;
+    while (c >= T.lvl_off[l + 1]) ++l;
+    const int sh = 3 * (L - l);
+    const uint64_t a = T.key[c] << sh, b = (T.key[c] + 1) << sh;
+    first[c] = lower_bound_key(T.key, leaf0, T.lvl_off[L + 1], a) - (int)leaf0;
+    end[c] = lower_bound_key(T.key, leaf0, T.lvl_off[L + 1], b) - (int)leaf0;
+    if (end[c] > first[c] && lrank[first[c]] == lrank[end[c] - 1]) owner[c] = lrank[first[c]];
+    has_src[c] = ppre[end[c]] > ppre[first[c]];
+  }
+  X.let_send.assign(R, {});
+  X.let_recv.assign(R, {});
+  X.let_shared.clear();
+  std::vector<char> need(nc);
+  for (int p = 0; p < R; ++p) {
+    std::fill(need.begin(), need.end(), 0);
+    const int a = (int)X.leaf_bounds[p], b = (int)X.leaf_bounds[p + 1];
+    for (int64_t c = c0; c < nc; ++c) {
+      const int f = std::max(first[c], a), e = std::min(end[c], b);
+      if (e <= f || tpre[e] == tpre[f]) continue;  // no targets of p below c
+      for (int k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k)
+        if (has_src[T.m2l_idx[k]]) need[T.m2l_idx[k]] = 1;
+    }
+    for (int64_t c = c0; c < nc; ++c) {
+      if (!need[c] || owner[c] < 0) continue;
+      if (p != me && owner[c] == me) X.let_send[p].push_back((int)c);
+      if (p == me && owner[c] != me) X.let_recv[owner[c]].push_back((int)c);
+    }
+  }
+  for (int64_t c = c0; c < nc; ++c)
+    if (owner[c] < 0 && has_src[c]) X.let_shared.push_back((int)c);
+}
+
+}  // namespace fmm
+
+using namespace fmm;
+
+struct fmmbem_plan {
+  HostTree tree;
+  ExchangePlan plan;
+};
+
+extern "C" {
+
+fmmbem_status fmmbem_plan_create(const uint64_t* leaf_keys, const int32_t* leaf_panels, const int32_t* leaf_charges,
+                                 int64_t n_leaves, int32_t level, int32_t quad_points, int32_t nranks, int32_t rank,
+                                 fmmbem_plan** out) {
+  if (out) *out = nullptr;
+  if (!out || !leaf_keys || !leaf_panels || n_leaves < 1 || level < 0 || level > MAX_LEVEL || nranks < 1 ||
+      nranks > 64 || rank < 0 || rank >= nranks || quad_points < 1)
+    return FMMBEM_E_INVALID;
+  for (int64_t k = 1; k < n_leaves; ++k)
+    if (!(leaf_keys[k - 1] < leaf_keys[k])) return FMMBEM_E_INVALID;
+  try {
+    auto* p = new fmmbem_plan();
+    host_tree(leaf_keys, n_leaves, level, p->tree);
+    std::vector<int> pan(leaf_panels, leaf_panels + n_leaves), tgt(pan);
+    if (leaf_charges)
+      for (int64_t k = 0; k < n_leaves; ++k) tgt[k] += leaf_charges[k];
+    plan_exchange(p->tree, pan, tgt, quad_points, nranks, rank, p->plan);
+    *out = p;
+    return FMMBEM_OK;
+  } catch (...) {
+    return FMMBEM_E_NOMEM;
+  }
+}
+
+void fmmbem_plan_destroy(fmmbem_plan* p) { delete p; }
+
+int64_t fmmbem_plan_list(const fmmbem_plan* p, int32_t list, int32_t peer, int64_t* out) {
+  if (!p) return -1;
+  const auto& X = p->plan;
+  const auto& T = p->tree;
+  const int R = (int)X.leaf_bounds.size() - 1;
+  auto emit = [&](const auto& v) -> int64_t {
+    if (out)
+      for (size_t i = 0; i < v.size(); ++i) out[i] = (int64_t)v[i];
+    return (int64_t)v.size();
+  };
+  const bool per_peer = list >= FMMBEM_PLAN_HALO_SEND && list <= FMMBEM_PLAN_LET_RECV;
+  if (per_peer && (peer < 0 || peer >= R)) return -1;
+  switch (list) {
+    case FMMBEM_PLAN_HALO_SEND: return emit(X.halo_send[peer]);
+    case FMMBEM_PLAN_HALO_RECV: return emit(X.halo_recv[peer]);
+    case FMMBEM_PLAN_LET_SEND: return emit(X.let_send[peer]);
+    case FMMBEM_PLAN_LET_RECV: return emit(X.let_recv[peer]);
+    case FMMBEM_PLAN_LET_SHARED: return emit(X.let_shared);
+    case FMMBEM_PLAN_LEAF_BOUNDS: return emit(X.leaf_bounds);
+    case FMMBEM_PLAN_CELL_KEYS: return emit(T.key);
+    case FMMBEM_PLAN_LEVEL_OFFSETS: return emit(T.lvl_off);
+    default: return -1;
+  }
+}
+
+}  // extern "C"

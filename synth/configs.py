@@ -96,7 +96,44 @@ def array(n=(10, 10, 10), nu: int = 113, spacing: float = 60.0, seed: int = 5,
     return _pack(V, T, C, Q, f"array_{n[0]}x{n[1]}x{n[2]}_nu{nu}")
 
 
+def array_part(n=(10, 10, 10), rank: int = 0, world: int = 1, nu: int = 113, spacing: float = 60.0,
+               seed: int = 5, jitter: float = 0.0, base=None):
+    """Rank `rank`'s part of the C5-style array for input_mode 1: the contiguous block of copies
+    [C r / world, C (r + 1) / world) (same rotations as `array`), ALL charges.  Concatenated in rank
+    order the parts are `array(...)`, so the library's global ids are the array's triangle indices."""
+    if base is None:
+        base = lysozyme(nu)
+    nc = n[0] * n[1] * n[2]
+    c0, c1 = nc * rank // world, nc * (rank + 1) // world
+    V, T, C, Q = replicate_grid(base["vertices"], base["triangles"], base["charge_xyz"], base["charge_q"], n,
+                                spacing, seed, jitter, copies=(c0, c1 - c0))
+    out = _pack(V, T, C, Q, f"array_{n[0]}x{n[1]}x{n[2]}_nu{nu}_part{rank}of{world}")
+    out["first_panel"] = c0 * len(base["triangles"])
+    out["n_panels_total"] = nc * len(base["triangles"])
+    return out
+
+
 def random_cube(n: int, seed: int = 0, width: float = 1.0):
     """Uniform random points in a cube (the paper's scaling control); points only."""
     rng = np.random.Generator(np.random.PCG64(seed))
     return rng.random((n, 3)) * width, rng.uniform(-1.0, 1.0, n)
+
+
+def cube_panels(n: int, seed: int = 0, width: float = 100.0, eps: float = 1e-4):
+    """The random-cube control ("N = 10^8 ... randomly distributed in a cube") as a
+    panel set the library accepts: one tiny right triangle (legs eps, far below the ~0.2 A mean
+    point spacing at 1e8 points in a 100 A cube) per uniform random point p, vertices
+    (p, p + eps e_x, p + eps e_y).  With the centroid rule a panel is a point source of weight
+    A_j x_j; `charge_per_area` = 1/A_j turns unit charges into x.  No charges."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    p = rng.random((n, 3)) * width
+    v = np.empty((n, 3, 3))
+    v[:, 0] = p
+    v[:, 1] = p
+    v[:, 1, 0] += eps
+    v[:, 2] = p
+    v[:, 2, 1] += eps
+    t = np.arange(3 * n, dtype=np.int64).reshape(n, 3)
+    out = _pack(v.reshape(-1, 3), t.astype(np.int32), np.zeros((0, 3)), np.zeros(0), f"random_cube_{n}")
+    out["charge_per_area"] = 2.0 / (eps * eps)
+    return out

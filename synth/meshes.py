@@ -178,12 +178,15 @@ def random_rotations(n: int, rng):
     return R
 
 
-def replicate_grid(v, tri, cxyz, cq, n=(10, 10, 10), spacing=60.0, seed=5, jitter=0.0):
+def replicate_grid(v, tri, cxyz, cq, n=(10, 10, 10), spacing=60.0, seed=5, jitter=0.0, copies=None,
+                   charges=True):
     """n[0]*n[1]*n[2] randomly rotated copies on a grid.
 
     Each copy is rotated about the origin (the molecule's frame) by an independent
     uniform random rotation and translated to its grid point (+ optional uniform
-    jitter of +-jitter Angstrom, "quasi-scattered").
+    jitter of +-jitter Angstrom, "quasi-scattered").  `copies` = (first, count)
+    materialises only that contiguous block of copies (the same rotations and positions as
+    the full array: a rank's part for input_mode 1); `charges` = False skips the charges.
     """
     rng = np.random.Generator(np.random.PCG64(seed))
     nx, ny, nz = n
@@ -196,15 +199,17 @@ def replicate_grid(v, tri, cxyz, cq, n=(10, 10, 10), spacing=60.0, seed=5, jitte
     shift = gi.reshape(-1, 3).astype(np.float64) * spacing
     if jitter > 0:
         shift += rng.uniform(-jitter, jitter, size=shift.shape)
+    c0, cn = (0, nc) if copies is None else copies
     nv, nt, ncg = len(v), len(tri), len(cxyz)
-    V = np.empty((nc, nv, 3))
-    C = np.empty((nc, ncg, 3))
-    for c in range(nc):  # per-copy rotation keeps peak memory at one copy of temporaries
-        np.matmul(v, R[c].T, out=V[c])
-        V[c] += shift[c]
+    V = np.empty((cn, nv, 3))
+    for i in range(cn):  # per-copy rotation keeps peak memory at one copy of temporaries
+        np.matmul(v, R[c0 + i].T, out=V[i])
+        V[i] += shift[c0 + i]
+    C = np.empty((nc if charges else 0, ncg, 3))
+    for c in range(len(C)):
         if ncg:
             np.matmul(cxyz, R[c].T, out=C[c])
             C[c] += shift[c]
-    T = (tri[None, :, :].astype(np.int64) + (np.arange(nc, dtype=np.int64) * nv)[:, None, None])
+    T = (tri[None, :, :].astype(np.int64) + (np.arange(cn, dtype=np.int64) * nv)[:, None, None])
     return (V.reshape(-1, 3), T.reshape(-1, 3).astype(np.int32), C.reshape(-1, 3),
-            np.tile(cq, nc))
+            np.tile(cq, len(C)))

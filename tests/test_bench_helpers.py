@@ -25,9 +25,9 @@ def test_m2l_flops_per_translation():
 
 def test_launches_per_matvec_c5():
     b = _bench()
-    # leaf level 8: P2M, 6 x (M2M rotate + sum), M2L, 6 L2L, P2P source table, P2P, L2P
-    assert b.launches_per_matvec(8, 12) == 1 + 2 * 6 + 1 + 6 + 1 + 1 + 1 == 23
-    assert b.launches_per_matvec(1, 12) == 2  # no far field: source table + P2P
+    # leaf level 8: P2M, 6 x (M2M rotate + sum), M2L, 6 L2L, P2P weight max + source table, P2P, L2P
+    assert b.launches_per_matvec(8, 13) == 1 + 2 * 6 + 1 + 6 + 2 + 1 + 1 == 24
+    assert b.launches_per_matvec(1, 13) == 3  # no far field: weight max + source table + P2P
 
 
 def test_p2p_flop_convention():

@@ -1,8 +1,13 @@
-"""Parity at the BASELINE.json configurations (full sizes, the bench launch configuration P = 12,
+"""Parity at the BASELINE.json configurations (full sizes, the bench launch configuration P = 13,
 leaf_points = 128), through the C ABI, against the FP64 oracle.
 
 Where the O(N^2) oracle is too slow for every output (C4, C5) it is evaluated on a seeded
 sample of rows (each row is the exact oracle sum over ALL sources).
+
+K' bounds: relative L2 <= 1e-4 (north star) and, per element,
+max_i |y_i - y_ref_i| <= 1e-3 max_i |y_ref_i| -- for random x and for the smooth / physical inputs
+GMRES applies (E_n, sigma, x = 1, low-order Y_lm).  Measured on a B200 at P = 12 the C3 random-x
+error is 1.4e-4 (smooth inputs <= 1.4e-5), at P = 13 7.0e-5: the bench order is 13.
 """
 import numpy as np
 import pytest
@@ -13,7 +18,7 @@ from oracle import bem, closed_forms as cf  # noqa: E402
 from synth import configs  # noqa: E402
 
 pytestmark = pytest.mark.gpu
-BENCH = dict(terms=12, leaf_points=128)
+BENCH = dict(terms=13, leaf_points=128)
 
 
 def solver(cfg, **kw):
@@ -25,6 +30,34 @@ def matvec_global(s, x, op):
     y = s.matvec(torch.tensor(s.to_local(x), dtype=torch.float32, device="cuda"), op)
     torch.cuda.synchronize()
     return s.to_global(y.cpu().numpy().astype(np.float64))
+
+
+def kprime_errors(y, ref):
+    e = y - ref
+    return float(np.linalg.norm(e) / np.linalg.norm(ref)), float(np.abs(e).max() / np.abs(ref).max())
+
+
+def input_vectors(P):
+    """Random x and the smooth / physical inputs of a K' matvec inside GMRES (rhs E_n, the solution
+    sigma, a constant, low-order spherical harmonics of the direction from the centre)."""
+    d = P.pan.centroid - P.pan.centroid.mean(0)
+    u = d / np.linalg.norm(d, axis=1)[:, None]
+    return {"rand": np.random.default_rng(31).normal(size=P.pan.n), "En": P.E.copy(), "one": np.ones(P.pan.n),
+            "y20": 1.5 * u[:, 2] ** 2 - 0.5, "y21": u[:, 0] * u[:, 2],
+            "y33": u[:, 0] * (u[:, 0] ** 2 - 3 * u[:, 1] ** 2), "sigma": P.solve("gmres")["sigma"]}
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_kprime_smooth_and_physical_inputs(name):
+    """the 1e-4 K' bound at the bench configuration for the vectors GMRES
+    actually applies, not only for white noise; plus a per-element bound."""
+    cfg = configs.kirkwood(64) if name == "c2" else configs.lysozyme(113)
+    P = bem.Problem(cfg)
+    s = solver(cfg, **BENCH)
+    errs = {}
+    for k, x in input_vectors(P).items():
+        errs[k] = kprime_errors(matvec_global(s, x, "kprime"), bem.apply_kprime(P.pan, x))
+    assert all(l2 < 1e-4 and mx < 1e-3 for l2, mx in errs.values()), errs
 
 
 def test_c1_born_fmm_and_direct():
@@ -89,16 +122,22 @@ def test_c4_binding_bibee_full_and_bem_scaled():
 
 
 def test_c5_array_sampled_rows():
+    """C5 (102,152,000 panels) at the bench launch configuration: K' on 1,024 seeded rows (each the
+    full FP64 sum over all sources) for random x, the per-molecule E_n field tiled over the copies
+    (the physical GMRES right-hand side) and x = 1; rel L2 and per-element bounds."""
     base = configs.lysozyme(113)
     cfg = configs.array((10, 10, 10), base=base)  # 102,152,000 panels
     s = solver(cfg, **BENCH)
     n = len(cfg["triangles"])
-    x = np.random.default_rng(23).normal(size=n)
-    y = matvec_global(s, x, "kprime")
-    rows = np.random.default_rng(24).choice(n, 64, replace=False)
+    pb = bem.Problem(base)
+    xs = {"rand": np.random.default_rng(23).normal(size=n), "En": np.tile(pb.E, n // pb.pan.n), "one": np.ones(n)}
+    rows = np.sort(np.random.default_rng(24).choice(n, 1024, replace=False))
     pan = bem.Panels(cfg["vertices"], cfg["triangles"])
-    ref = bem.apply_kprime(pan, x, rows=rows)
-    assert bem.rel_l2(y[rows], ref) < 1e-4
-    # every output finite, deterministic repeat
-    assert np.isfinite(y).all()
-    assert np.array_equal(y, matvec_global(s, x, "kprime"))
+    errs = {}
+    for k, x in xs.items():
+        y = matvec_global(s, x, "kprime")
+        errs[k] = kprime_errors(y[rows], bem.apply_kprime(pan, x, rows=rows))
+        if k == "rand":  # every output finite, deterministic repeat
+            assert np.isfinite(y).all()
+            assert np.array_equal(y, matvec_global(s, x, "kprime"))
+    assert all(l2 < 1e-4 and mx < 1e-3 for l2, mx in errs.values()), errs

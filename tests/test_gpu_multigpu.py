@@ -1,6 +1,7 @@
-"""Multi-GPU parity: the octree domain decomposition over NCCL reproduces the
-single-GPU matvec (also with the curvature self-term), GMRES solve and BIBEE energy, and the
-host-buffer product equals the device one.  Needs >= 2 GPUs (skipped otherwise)."""
+"""Multi-GPU parity: the octree domain decomposition over NCCL -- halo exchange of the
+near-field weights, LET multipoles -- reproduces the single-GPU matvec, GMRES solve, BIBEE energy and
+reaction potential, with the full mesh on every rank (input_mode 0) and with every rank passing only
+its part (input_mode 1), and with the self-term / analytic near-field options.  Needs >= 2 GPUs."""
 import json
 import os
 import subprocess
@@ -13,20 +14,28 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("case", ["lyso40", "c3"])
-def test_two_gpus_match_one(case):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+def run_check(case, n):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + (os.getpid() % 200)),
            os.path.join(ROOT, "tools", "mgpu_check.py"), case]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     line = [l for l in out.stdout.splitlines() if l.startswith("MGPU ")]
     assert line, out.stdout[-2000:] + out.stderr[-2000:]
-    r = json.loads(line[0][5:])
-    assert r["matvec_rel"] < 1e-6
-    assert r["self_term_rel"] < 1e-6  # option self_term = 1 on the domain decomposition
-    assert r["host_rel"] == 0.0  # host-buffer product = device product (same path on N > 1)
-    g, o, gi, oi = r["solve"]
-    assert abs(g / o - 1) < 1e-6 and abs(gi - oi) <= 1
-    assert abs(r["bibee"][0] / r["bibee"][1] - 1) < 1e-6
-    assert min(r["n_local"]) > 0
+    return json.loads(line[0][5:])
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("case", ["lyso40", "c3"])
+def test_two_gpus_match_one(case):
+    r = run_check(case, 2)
+    for rk in r["ranks"]:
+        for mode in ("mode0", "mode1"):
+            m = rk[mode]
+            assert m["n_local"] > 0
+            assert m["matvec_rel"] < 1e-6, m
+            assert m["host_rel"] == 0.0, m  # host-buffer product = device product (same path on N > 1)
+            g, o, gi, oi = m["solve"]
+            assert abs(g / o - 1) < 1e-6 and abs(gi - oi) <= 1, m
+            assert abs(m["bibee"][0] / m["bibee"][1] - 1) < 1e-6, m
+            assert m["phi_rel"] < 1e-6, m
+        assert rk["self_term"] < 1e-6 and rk["near_mode_leaf_points"] < 1e-6, rk

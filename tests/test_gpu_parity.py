@@ -201,7 +201,7 @@ def test_single_panel_and_no_charges():
     assert s.bibee("cfa")["dG"] == 0.0
 
 
-@pytest.mark.parametrize("terms", [8, 10, 12])
+@pytest.mark.parametrize("terms", [8, 10, 12, 13, 14])
 def test_rotation_m2l_equals_plain_translation(problems, monkeypatch, terms):
     """The O(P^3) rotation M2L and the plain O(P^4) translation are the same
     operator: their matvecs agree to FP32 rounding."""

@@ -1,56 +1,94 @@
-"""Multi-GPU parity check (run under torchrun): the distributed matvec / solve / BIBEE equal the
-single-GPU results.  Not a pytest (needs N GPUs); tests/test_gpu_multigpu.py drives it."""
-import os, sys, json
+"""Multi-GPU parity check (run under torchrun): the distributed matvec / solve / BIBEE / reaction
+potential equal the single-GPU results, for input_mode 0 (full mesh on every rank) and 1 (every rank
+passes only its part of the mesh), with the self-term and analytic near-field options (mode 0).
+Not a pytest (needs N GPUs); tests/test_gpu_multigpu.py drives it."""
+import json
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import torch.distributed as dist
+
 from paper_1007_4591_b200 import Solver
 from synth import configs
 
-rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-torch.cuda.set_device(local)
-dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-name = sys.argv[1] if len(sys.argv) > 1 else "lyso40"
-cfg = {"lyso40": lambda: configs.lysozyme(40, 400), "kirk32": lambda: configs.kirkwood(32),
-       "c3": lambda: configs.lysozyme(113)}[name]()
-opts = dict(terms=12, leaf_points=32, device=local)
-s = Solver.distributed(cfg, **opts)
-n = len(cfg["triangles"])
-x = np.random.default_rng(3).normal(size=n)
-y = s.matvec(torch.tensor(x[s.local_ids], dtype=torch.float32, device="cuda"), "kprime")
-torch.cuda.synchronize()
-parts = [None] * world
-dist.all_gather_object(parts, (s.local_ids, y.cpu().numpy()))
-yh = s.matvec_host(x[s.local_ids].astype(np.float32), "kprime")  # plain host-buffer path (N > 1)
-host_rel = float(np.linalg.norm(yh - y.cpu().numpy()) / np.linalg.norm(y.cpu().numpy()))
-s_st = Solver.distributed(cfg, self_term=1, **opts)  # curvature self-term option (A7) across ranks
-y_st = s_st.matvec(torch.tensor(x[s_st.local_ids], dtype=torch.float32, device="cuda"), "A")
-torch.cuda.synchronize()
-parts_st = [None] * world
-dist.all_gather_object(parts_st, (s_st.local_ids, y_st.cpu().numpy(), host_rel))
-r = s.solve()
-b = s.bibee("cfa")
-out = {}
-if rank == 0:
-    yd = np.empty(n)
+
+def part_of(cfg, rank, world):
+    """Rank's contiguous block of triangles with its own (compacted) vertex array: global ids of
+    input_mode 1 are then the triangle indices."""
+    t = cfg["triangles"]
+    n = len(t)
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    tt = t[lo:hi]
+    used, inv = np.unique(tt.reshape(-1), return_inverse=True)
+    return dict(cfg, vertices=cfg["vertices"][used], triangles=inv.reshape(-1, 3).astype(np.int32))
+
+
+def gather(s, y):
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, (s.local_ids, y.cpu().numpy()))
+    n = sum(len(p[0]) for p in parts)
+    out = np.empty(n)
     for ids, yy in parts:
-        yd[ids] = yy
-    s1 = Solver.from_config(cfg, terms=12, leaf_points=32, device=local)
-    y1 = s1.to_global(s1.matvec(torch.tensor(s1.to_local(x), dtype=torch.float32, device="cuda"), "kprime").cpu().numpy())
+        out[ids] = yy
+    return out
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = sys.argv[1] if len(sys.argv) > 1 else "lyso40"
+    cfg = {"lyso40": lambda: configs.lysozyme(40, 400), "kirk32": lambda: configs.kirkwood(32),
+           "c3": lambda: configs.lysozyme(113)}[name]()
+    opts = dict(terms=13, leaf_points=32, device=local)
+    n = len(cfg["triangles"])
+    x = np.random.default_rng(3).normal(size=n)
+    res = {}
+    # single-GPU reference (every rank computes it: simple and symmetric)
+    s1 = Solver.from_config(cfg, **opts)
+    dev = lambda s, v: torch.tensor(v[s.local_ids], dtype=torch.float32, device="cuda")
+    y1 = s1.to_global(s1.matvec(dev(s1, x), "kprime").cpu().numpy())
     r1 = s1.solve()
     b1 = s1.bibee("cfa")
-    yst = np.empty(n)
-    for ids, yy, _ in parts_st:
-        yst[ids] = yy
-    s1st = Solver.from_config(cfg, self_term=1, terms=12, leaf_points=32, device=local)
-    y1st = s1st.to_global(s1st.matvec(torch.tensor(s1st.to_local(x), dtype=torch.float32, device="cuda"),
-                                       "A").cpu().numpy())
-    out = dict(world=world, n_local=[len(p[0]) for p in parts],
-               matvec_rel=float(np.linalg.norm(yd - y1) / np.linalg.norm(y1)),
-               self_term_rel=float(np.linalg.norm(yst - y1st) / np.linalg.norm(y1st)),
-               host_rel=max(p[2] for p in parts_st),
-               solve=(r["dG"], r1["dG"], r["iterations"], r1["iterations"]), bibee=(b["dG"], b1["dG"]))
-    print("MGPU", json.dumps(out), flush=True)
-dist.barrier()
-dist.destroy_process_group()
+    phi1 = s1.reaction_potential(r1["sigma"])
+    for mode in (0, 1):
+        c = cfg if mode == 0 else part_of(cfg, rank, world)
+        s = Solver.distributed(c, input_mode=mode, **opts)
+        y = gather(s, s.matvec(dev(s, x), "kprime"))
+        yh = s.matvec_host(x[s.local_ids].astype(np.float32), "kprime")
+        r = s.solve()
+        b = s.bibee("cfa")
+        sig = gather(s, r["sigma"])
+        phi = s.reaction_potential(torch.tensor(sig[s.local_ids], dtype=torch.float32, device="cuda"))
+        res[f"mode{mode}"] = dict(n_local=s.n, matvec_rel=rel(y, y1),
+                                  host_rel=float(np.abs(yh - y[s.local_ids]).max()),
+                                  solve=(r["dG"], r1["dG"], r["iterations"], r1["iterations"]),
+                                  bibee=(b["dG"], b1["dG"]), phi_rel=rel(phi, phi1))
+        s.close()
+    # options that need the full mesh (input_mode 0): curvature self-term, analytic near field
+    for kw in (dict(self_term=1), dict(near_mode=1, leaf_points=64)):
+        o = dict(opts, **kw)
+        sr = Solver.from_config(cfg, **o)
+        yr = sr.to_global(sr.matvec(dev(sr, x), "A").cpu().numpy())
+        s = Solver.distributed(cfg, **o)
+        y = gather(s, s.matvec(dev(s, x), "A"))
+        res["_".join(kw)] = rel(y, yr)
+        s.close()
+        sr.close()
+    allr = [None] * world
+    dist.all_gather_object(allr, res)
+    if rank == 0:
+        print("MGPU", json.dumps(dict(world=world, ranks=allr)), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
