@@ -406,3 +406,47 @@ def test_near_operator_consistency():
     assert abs(np.mean(bem.apply_kprime_near(p, x)) + 0.5) < 0.03
     # the single-layer self term of a flat panel is positive and O(sqrt(A))
     assert np.all(self_pot > 0) and np.allclose(self_pot / np.sqrt(p.area), self_pot[0] / np.sqrt(p.area[0]), rtol=0.3)
+
+
+# ---------------------------------------------------------------- round-2 pins
+
+def test_near_pairs_equal_brute_force_on_a_tiny_mesh():
+    """near_pairs (KD-tree query + filter) equals the O(n^2) brute-force enumeration of its definition
+    j != i, |c_i - c_j| < eta sqrt(A_j) on a small irregular mesh (different areas per panel)."""
+    cfg = configs.lysozyme(nu=6, n_atoms=10)
+    p = bem.Panels(cfg["vertices"], cfg["triangles"])
+    for eta in (1.0, 2.5, 4.0):
+        i, j = bem.near_pairs(p, eta)
+        d = np.linalg.norm(p.centroid[:, None, :] - p.centroid[None, :, :], axis=2)
+        want = set(zip(*np.nonzero((d < eta * np.sqrt(p.area)[None, :]) & ~np.eye(p.n, dtype=bool))))
+        got = set(zip(i.tolist(), j.tolist()))
+        assert got == want and len(want) > 0
+        assert not any(a == b for a, b in got)
+
+
+def test_charge_potential_mean_value_on_a_sphere():
+    """psi_i = sum_k q_k G(c_i, r_k): by the shell theorem the area-weighted sum over a sphere of
+    radius a of the potential of an interior unit charge is q a (independent of the charge's
+    position inside); the flat-panel centroid rule converges to it with refinement."""
+    errs = []
+    for nu in (8, 16, 32):
+        cfg = configs.born(nu, radius=2.0)
+        p = bem.Panels(cfg["vertices"], cfg["triangles"])
+        for r in ([0.0, 0.0, 0.0], [0.3, -0.5, 0.7]):
+            psi = bem.charge_potential(p, np.array([r]), np.array([1.0]))
+            errs.append(abs(np.sum(p.area * psi) / 2.0 - 1.0))
+    assert errs[-1] < 2e-4 and errs[-2] < 2e-4
+    assert errs[-1] < errs[-3] < errs[1]  # monotone in nu (off-centre charge)
+    assert 3.0 < errs[-3] / errs[-1] < 5.0  # second order in the panel size
+
+
+def test_rows_helpers_equal_full_operators():
+    """KprimeRows / SingleRows (the split used to time the oracle) give the rows of the full sums."""
+    cfg = configs.kirkwood(6)
+    p = bem.Panels(cfg["vertices"], cfg["triangles"], K=3)
+    x = np.random.default_rng(3).normal(size=p.n)
+    rows = np.array([0, 5, 17, p.n - 1])
+    assert np.array_equal(bem.KprimeRows(p, x)(rows), bem.apply_kprime(p, x)[rows])
+    assert np.array_equal(bem.SingleRows(p, x)(rows), bem.apply_single(p, x)[rows])
+    En = bem.normal_field(p, cfg["charge_xyz"], cfg["charge_q"], 4.0)
+    assert np.array_equal(bem.normal_field(p, cfg["charge_xyz"], cfg["charge_q"], 4.0, rows=rows), En[rows])

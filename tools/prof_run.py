@@ -9,7 +9,7 @@ import bench
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
 ap.add_argument("--reps", type=int, default=3)
-ap.add_argument("--terms", type=int, default=12)
+ap.add_argument("--terms", type=int, default=13)
 ap.add_argument("--leaf-points", type=int, default=128)
 ap.add_argument("--op", default="A")
 a = ap.parse_args()
