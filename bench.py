@@ -355,18 +355,21 @@ def main():
         torch.cuda.synchronize()
         s.reset_fields()
         bib = s.bibee("cfa")  # first call: allocations + work lists
-        bms = []
+        bms, bph = [], []
         for _ in range(args.bibee_calls):
             s.reset_fields()
             bib = s.bibee("cfa")
-            bms.append(s.timing()["bibee"])
+            tb = s.timing()  # the charge-FMM's phases (until the next matvec)
+            bms.append(tb["bibee"])
+            bph.append({k: tb[k] for k in ("upward", "m2l", "p2p", "l2p", "total")})
         bms = float(np.mean(bms))
         if dist:
             t = torch.tensor([bms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             bms = float(t.item())
         bibee = {"dG_kcal_mol": bib["dG_kcal"], "dG_internal": bib["dG"], "ms": bms, "calls": args.bibee_calls,
-                 "energies_per_s": 1e3 / bms}
+                 "energies_per_s": 1e3 / bms,
+                 "charge_fmm_phases_ms": {k: float(np.mean([b[k] for b in bph])) for k in bph[0]}}
 
     p2p_int = int(tm["p2p_interactions"])
     p2p_s = ph["p2p"] * 1e-3

@@ -380,7 +380,13 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
     o.pot.y = c->psi.get() - c->pan_lo;
     o.pot.b = (float)(1.0 / FOUR_PI);
   }
-  fmm_eval(c, t, s, o, false, true, st, false, false);
+  // phase events of this charge-FMM (fmmbem_last_timing reports them until the next matvec)
+  cudaEventRecord(c->ev[E_AG0], st);
+  fmm_eval(c, t, s, o, false, true, st, true, false);
+  cudaEventRecord(c->ev[E_NEAR1], st);
+  c->timed_near = true;
+  c->timed_comm = false;
+  c->timed_xg = false;
   if (c->K > 1) {
     DevBuf<float> psiq;
     psiq.alloc(c->quad.n);

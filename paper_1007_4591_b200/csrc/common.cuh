@@ -18,12 +18,13 @@ struct Error : std::runtime_error {
   Error(fmmbem_status c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
-#define FMM_CUDA(call)                                                                   \
-  do {                                                                                   \
-    cudaError_t e_ = (call);                                                             \
-    if (e_ != cudaSuccess)                                                               \
-      throw ::fmm::Error(e_ == cudaErrorMemoryAllocation ? FMMBEM_E_NOMEM : FMMBEM_E_CUDA, \
-                         std::string(#call) + ": " + cudaGetErrorString(e_));           \
+#define FMM_CUDA(call)                                                                                    \
+  do {                                                                                                    \
+    cudaError_t e_ = (call);                                                                              \
+    if (e_ != cudaSuccess)                                                                                \
+      throw ::fmm::Error(e_ == cudaErrorMemoryAllocation ? FMMBEM_E_NOMEM : FMMBEM_E_CUDA,                \
+                         std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + __FILE__ + ":" +     \
+                             std::to_string(__LINE__) + ")");                                             \
   } while (0)
 
 #define FMM_CHECK_LAUNCH() FMM_CUDA(cudaGetLastError())

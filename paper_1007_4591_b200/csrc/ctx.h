@@ -33,7 +33,8 @@ struct Tree {
   DevBuf<int> child_begin, child_end;  // [n_cells] global child range (level + 1)
   DevBuf<int4> leaf_ijk;         // [n_leaves] integer leaf coordinates
   DevBuf<int> nbr_off, nbr_idx;  // leaf-level neighbour CSR (leaf indices, incl. self)
-  DevBuf<int> m2l_off, m2l_idx;  // [n_cells+1] interaction-list CSR (global source cell idx)
+  DevBuf<long long> m2l_off;     // [n_cells+1] interaction-list CSR offsets (64-bit: > 2^31 entries at 1e9 panels)
+  DevBuf<int> m2l_idx;           // global source cell index of each interaction-list entry
   int64_t nbr_pairs = 0, m2l_pairs = 0;
   double width(int l) const { return W / (double)(1LL << l); }
 };

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(64) k_m2m(int lvl_off, int P, const int* __res
 constexpr int M2L_TPB = 64;
 constexpr int M2L_SB = 4;  // sources staged per step
 
-__global__ void __launch_bounds__(M2L_TPB) k_m2l(int cell_off, int P, const int* __restrict__ off,
+__global__ void __launch_bounds__(M2L_TPB) k_m2l(int cell_off, int P, const long long* __restrict__ off,
                                                  const int* __restrict__ idx, const uint64_t* __restrict__ key,
                                                  const int* __restrict__ scnt, const int* __restrict__ tcnt,
                                                  const float2* __restrict__ M, const float2* __restrict__ Itab,
@@ -177,14 +177,14 @@ __global__ void __launch_bounds__(M2L_TPB) k_m2l(int cell_off, int P, const int*
   float2* If = sm + M2L_SB * NF;      // [SB][NIF]  full I(delta)
   const int cell = cell_off + blockIdx.x;
   if (tcnt[cell] == 0) return;
-  const int lo = off[cell], hi = off[cell + 1];
+  const long long lo = off[cell], hi = off[cell + 1];
   if (lo == hi) return;
   int tx, ty, tz;
   demorton(key[cell], tx, ty, tz);
   // outputs owned by this thread (up to 3 for P <= 16)
   float2 acc[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  for (int e0 = lo; e0 < hi; e0 += M2L_SB) {
-    const int ns = min(M2L_SB, hi - e0);
+  for (long long e0 = lo; e0 < hi; e0 += M2L_SB) {
+    const int ns = (int)min((long long)M2L_SB, hi - e0);
     __syncthreads();
     for (int q = 0; q < ns; ++q) {
       const int s = idx[e0 + q];

@@ -632,18 +632,18 @@ double wigner_d(int n, int mp, int m, double b) {
 }
 
 // compacted interaction lists (sources with points of `src`, targets with points of `tgt`)
-__global__ void k_compact_count(int n, int cell_off, const int* __restrict__ off, const int* __restrict__ idx,
+__global__ void k_compact_count(int n, int cell_off, const long long* __restrict__ off, const int* __restrict__ idx,
                                 const int* __restrict__ scnt, const int* __restrict__ tcnt, int* cnt) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int c = cell_off + i;
   int m = 0;
   if (tcnt[c] > 0)
-    for (int e = off[c]; e < off[c + 1]; ++e) m += scnt[idx[e]] > 0;
+    for (long long e = off[c]; e < off[c + 1]; ++e) m += scnt[idx[e]] > 0;
   cnt[i] = m;
 }
 
-__global__ void k_compact_fill(int n, int cell_off, const int* __restrict__ off, const int* __restrict__ idx,
+__global__ void k_compact_fill(int n, int cell_off, const long long* __restrict__ off, const int* __restrict__ idx,
                                const int* __restrict__ scnt, const int* __restrict__ pos, int* out_idx,
                                int* out_cell, int* out_off) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -652,7 +652,7 @@ __global__ void k_compact_fill(int n, int cell_off, const int* __restrict__ off,
   const int start = pos[i], end = pos[i + 1];
   if (start == end) return;
   int w = start;
-  for (int e = off[c]; e < off[c + 1]; ++e)
+  for (long long e = off[c]; e < off[c + 1]; ++e)
     if (scnt[idx[e]] > 0) out_idx[w++] = idx[e];
   // row r of the compacted list = number of non-empty rows before i
   out_cell[pos[n + 1 + i]] = c;

@@ -96,7 +96,7 @@ void host_tree(const uint64_t* leaf_keys, int64_t nl, int L, HostTree& T) {
             }
           }
     }
-    T.m2l_off[c + 1] = (int)T.m2l_idx.size();
+    T.m2l_off[c + 1] = (int64_t)T.m2l_idx.size();
   }
 }
 
@@ -168,7 +168,7 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
     for (int64_t c = c0; c < nc; ++c) {
       const int f = std::max(first[c], a), e = std::min(end[c], b);
       if (e <= f || tpre[e] == tpre[f]) continue;  // no targets of p below c
-      for (int k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k)
+      for (int64_t k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k)
         if (has_src[T.m2l_idx[k]]) need[T.m2l_idx[k]] = 1;
     }
     for (int64_t c = c0; c < nc; ++c) {

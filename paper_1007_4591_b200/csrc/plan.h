@@ -16,7 +16,8 @@ struct HostTree {
   std::vector<uint64_t> key;
   std::vector<int> child_b, child_e;
   std::vector<int> nbr_off, nbr_idx;
-  std::vector<int> m2l_off, m2l_idx;
+  std::vector<int64_t> m2l_off;
+  std::vector<int> m2l_idx;
 };
 
 struct ExchangePlan {

@@ -11,7 +11,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ctx.h"
 #include "kernels.cuh"
@@ -185,14 +188,15 @@ __global__ void k_nbr(int nl, const uint64_t* __restrict__ lkey, const int4* __r
 __global__ void k_m2l_list(int n, const uint64_t* __restrict__ key, int lvl_off, int par_n,
                            const uint64_t* __restrict__ pkey, int par_off, const int* __restrict__ cb,
                            const int* __restrict__ ce, const uint64_t* __restrict__ allkey, int l,
-                           const int* __restrict__ off, int* cnt_or_idx, int pass) {
+                           const long long* __restrict__ off, int* cnt_or_idx, int pass) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int x, y, z;
   demorton(key[i], x, y, z);
   int px = x >> 1, py = y >> 1, pz = z >> 1;
   int lim = 1 << (l - 1);
-  int o = pass ? off[lvl_off + i] : 0, m = 0;
+  long long o = pass ? off[lvl_off + i] : 0;
+  int m = 0;
   for (int dz = -1; dz <= 1; ++dz)
     for (int dy = -1; dy <= 1; ++dy)
       for (int dx = -1; dx <= 1; ++dx) {
@@ -400,6 +404,11 @@ __global__ void k_local_counts(int nl, const int* __restrict__ gbeg, const int* 
   cnt[k] = present ? gbeg[k + 1] - gbeg[k] : 0;
 }
 
+__global__ void k_widen(int n, const int* __restrict__ in, long long* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
 __global__ void k_point_leaf_off(int nl, const int* __restrict__ begin, int leaf_off, int* leaf) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nl) return;
@@ -521,6 +530,17 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
   const int R = c->nranks, me = c->rank, K = c->K;
   const int64_t m = in.n, nc = c->nc;
   const int TB = 256;
+  // FMMBEM_VERBOSE=1: host-clock time of each setup stage on stderr (synchronising the stream)
+  static const bool verbose = std::getenv("FMMBEM_VERBOSE") != nullptr;
+  auto t_stage = std::chrono::steady_clock::now();
+  auto stage = [&](const char* name) {
+    if (!verbose) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[fmmbem rank %d] %-12s %8.1f ms\n", me, name,
+                 std::chrono::duration<double, std::milli>(now - t_stage).count());
+    t_stage = now;
+  };
   // 1. root cube: bounding cube of all ranks' centroids and the (replicated) charges
   double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
   bbox(in.cen, m, mn, mx, s);
@@ -548,6 +568,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
   for (int d = 0; d < 3; ++d) T.x0[d] = 0.5 * (mn[d] + mx[d]) - 0.5 * T.W;
   const double inv_h21 = (double)(1 << MAX_LEVEL) / T.W;
 
+  stage("bbox");
   // 2. Morton keys at depth 21 + stable radix sort (ties keep the input order)
   DevBuf<uint64_t> kp;
   DevBuf<int> pperm;
@@ -573,6 +594,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     sort_pairs(kc_in, ic_in, kc, cperm, nc, s);
   }
 
+  stage("keys+sort");
   // 3. leaf level: the smallest L with (global panels) / (occupied cells at L) <= leaf_points
   int64_t np = m;
   if (R > 1) {
@@ -626,6 +648,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
   T.L = L;
   const int shift = 3 * (MAX_LEVEL - L);
 
+  stage("leaf level");
   // 4. leaf skeleton = panel cells U charge cells (charges replicated), panel count per leaf
   std::vector<DevBuf<uint64_t>> lvl(L + 1);
   std::vector<int64_t> nlev(L + 1);
@@ -686,6 +709,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
   T.leaf_ijk.alloc(nl);
   k_leaf_ijk<<<ceil_div(nl, TB), TB, 0, s>>>(nl, lvl[L].get(), T.leaf_ijk.get());
   FMM_CHECK_LAUNCH();
+  stage("skeleton");
   // global panel CSR over the leaves
   c->gbeg.alloc(nl + 1);
   {
@@ -714,6 +738,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     FMM_CHECK_LAUNCH();
   }
   {
+    // interaction-list offsets are 64-bit: ~100 entries per cell exceed 2^31 beyond ~2e7 cells (22^3 array)
     int nC = (int)T.n_cells;
     DevBuf<int> cnt;
     cnt.alloc(nC + 1);
@@ -723,13 +748,17 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
                                                       lvl[l - 1].get(), (int)T.lvl_off[l - 1], T.child_begin.get(),
                                                       T.child_end.get(), T.key.get(), l, nullptr, cnt.get(), 0);
     FMM_CHECK_LAUNCH();
+    DevBuf<long long> cnt64;
+    cnt64.alloc(nC + 1);
+    k_widen<<<ceil_div(nC + 1, TB), TB, 0, s>>>(nC + 1, cnt.get(), cnt64.get());
+    FMM_CHECK_LAUNCH();
     T.m2l_off.alloc(nC + 1);
-    exclusive_scan(cnt.get(), T.m2l_off.get(), nC + 1, s);
-    int tot = 0;
-    FMM_CUDA(cudaMemcpyAsync(&tot, T.m2l_off.get() + nC, sizeof(int), cudaMemcpyDeviceToHost, s));
+    exclusive_scan(cnt64.get(), T.m2l_off.get(), nC + 1, s);
+    long long tot = 0;
+    FMM_CUDA(cudaMemcpyAsync(&tot, T.m2l_off.get() + nC, sizeof(long long), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaStreamSynchronize(s));
     T.m2l_pairs = tot;
-    T.m2l_idx.alloc(std::max(tot, 1));
+    T.m2l_idx.alloc(std::max<long long>(tot, 1));
     for (int l = 2; l <= L; ++l)
       k_m2l_list<<<ceil_div(nlev[l], TB), TB, 0, s>>>((int)nlev[l], lvl[l].get(), (int)T.lvl_off[l], (int)nlev[l - 1],
                                                       lvl[l - 1].get(), (int)T.lvl_off[l - 1], T.child_begin.get(),
@@ -738,6 +767,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     FMM_CHECK_LAUNCH();
   }
 
+  stage("lists");
   // charges (replicated): their leaf CSR (the targets of the reaction potential count in the LET)
   auto& C = c->chg;
   C.n = nc;
@@ -760,7 +790,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     FMM_CUDA(cudaMemcpyAsync(H.key.data(), T.key.get(), T.n_cells * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(H.nbr_off.data(), T.nbr_off.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(H.nbr_idx.data(), T.nbr_idx.get(), T.nbr_pairs * sizeof(int), cudaMemcpyDeviceToHost, s));
-    FMM_CUDA(cudaMemcpyAsync(H.m2l_off.data(), T.m2l_off.get(), (T.n_cells + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaMemcpyAsync(H.m2l_off.data(), T.m2l_off.get(), (T.n_cells + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(H.m2l_idx.data(), T.m2l_idx.get(), T.m2l_pairs * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(gb.data(), c->gbeg.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(cb.data(), C.begin.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -793,6 +823,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
   FMM_CUDA(cudaStreamSynchronize(s));
   const int64_t n_own = hgb[leaf_hi] - hgb[leaf_lo];
 
+  stage("plan");
   // 6. panels to their owners: FP64 records in the slice's key order, one contiguous segment per rank
   const int Wd = 9 + (K > 1 ? 3 * K : 0);
   DevBuf<unsigned long long> orec;  // owned records, Morton order
@@ -876,6 +907,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     }
     FMM_CUDA(cudaStreamSynchronize(s));
   }
+  stage("migration");
   // duplicate centroids (always in one leaf, hence on one rank; the verdict is made collective)
   {
     DevBuf<long long> f;
@@ -899,6 +931,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     if (fd < 1e300) throw Error(FMMBEM_E_COINCIDENT, "duplicate panel centroid at triangle " + std::to_string((long long)fd));
   }
 
+  stage("dup check");
   // 7. owned point data (leaf-local FP32), then the near-field halo
   const double h = T.width(L);
   DevBuf<float4> opos, onrm, oquad;
@@ -966,6 +999,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     FMM_CUDA(cudaStreamSynchronize(s));
   }
 
+  stage("points+halo");
   // 8. charges (replicated): tree order, leaf-local coordinates
   if (nc) {
     C.pos.alloc(nc);
@@ -978,6 +1012,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     FMM_CUDA(cudaMemcpyAsync(c->chg_ids.get(), cperm.get(), nc * sizeof(int), cudaMemcpyDeviceToDevice, s));
   }
 
+  stage("charges");
   // 9. subtree counts: panels of ALL ranks (sources: a cell with any panel has a multipole), charges
   {
     auto up = [&](DevBuf<int>& cnt, const int* beg, int mult, int lo, int hi) {
@@ -998,6 +1033,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     }
   }
   FMM_CUDA(cudaStreamSynchronize(s));
+  stage("counts");
 }
 
 // Near-field halo (SURVEY 8(e) per-apply step 1): which owned leaves each peer's P2P needs and which
