@@ -361,7 +361,7 @@ def main():
             bib = s.bibee("cfa")
             tb = s.timing()  # the charge-FMM's phases (until the next matvec)
             bms.append(tb["bibee"])
-            bph.append({k: tb[k] for k in ("upward", "m2l", "p2p", "l2p", "total")})
+            bph.append({k: tb[k] for k in ("upward", "m2l", "p2p", "l2p", "total", "p2p_interactions")})
         bms = float(np.mean(bms))
         if dist:
             t = torch.tensor([bms], device="cuda")

@@ -354,6 +354,7 @@ void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_
   }
   if (timing) cudaEventRecord(c->ev[E_NEAR1], st);
   c->timed_near = timing;
+  c->timed_fields = false;
 }
 
 void apply_A(fmmbem_ctx* c, const float* x, float* y, cudaStream_t s) { apply_op(c, FMMBEM_OP_A, x, y, s, false); }
@@ -381,12 +382,17 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
     o.pot.b = (float)(1.0 / FOUR_PI);
   }
   // phase events of this charge-FMM (fmmbem_last_timing reports them until the next matvec)
+  if (c->p2p_inter_chg < 0 && c->tree.L >= 2 && !c->opt.direct)
+    c->p2p_inter_chg = count_p2p(c, c->pan, c->chg, false, false, c->leaf_lo, c->leaf_hi);
   cudaEventRecord(c->ev[E_AG0], st);
-  fmm_eval(c, t, s, o, false, true, st, true, false);
+  // the charge-on-panel-point check (A14) depends on the geometry only: done at the first evaluation
+  const bool check = !c->fields_checked;
+  fmm_eval(c, t, s, o, false, check, st, true, false);
   cudaEventRecord(c->ev[E_NEAR1], st);
   c->timed_near = true;
   c->timed_comm = false;
   c->timed_xg = false;
+  c->timed_fields = true;
   if (c->K > 1) {
     DevBuf<float> psiq;
     psiq.alloc(c->quad.n);
@@ -394,7 +400,7 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
     Outputs oq;
     oq.pot.y = psiq.get();
     oq.pot.b = (float)(1.0 / FOUR_PI);
-    fmm_eval(c, tq, s, oq, false, true, st, false, false);
+    fmm_eval(c, tq, s, oq, false, check, st, false, false);
     if (n > 0)
       k_quad_reduce<<<ceil_div(n, 256), 256, 0, st>>>(n, c->K, psiq.get() + c->pan_lo * c->K,
                                                       c->quad.pos.get() + c->pan_lo * c->K,
@@ -405,7 +411,17 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
   int flag = 0;
   FMM_CUDA(cudaMemcpyAsync(&flag, c->flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
+  if (check && multi(c)) {  // the verdict is collective: every rank throws or none does
+    double f = flag ? 1.0 : 0.0;
+    c->red.alloc(std::max<size_t>(c->red.n, 64));
+    FMM_CUDA(cudaMemcpyAsync(c->red.get(), &f, sizeof(f), cudaMemcpyHostToDevice, st));
+    comm_allreduce_f64(c, c->red.get(), 1, st);
+    FMM_CUDA(cudaMemcpyAsync(&f, c->red.get(), sizeof(f), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+    flag = f > 0.0;
+  }
   if (flag) throw Error(FMMBEM_E_COINCIDENT, "a charge coincides with a panel quadrature point");
+  c->fields_checked = true;
   c->have_fields = true;
 }
 
@@ -435,7 +451,7 @@ void fill_timing(fmmbem_ctx* c, bool direct) {
   T.near = el(E_L2P1, E_NEAR1);
   if (c->timed_comm) T.comm = el(E_AR0, E_AR1) + (c->timed_xg ? el(E_XG0, E_XG1) : el(E_AG0, E_AG1));
   T.total = el(E_AG0, E_NEAR1);  // wall time of the whole product (overlapped phases counted once)
-  T.p2p_interactions = c->p2p_inter_kp;
+  T.p2p_interactions = c->timed_fields ? c->p2p_inter_chg : c->p2p_inter_kp;
   T.m2l_pairs = direct ? 0 : c->m2l_pairs_kp;
 }
 
@@ -553,7 +569,9 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   if (const char* e = std::getenv("FMMBEM_P2P_CHUNK")) c->p2p_chunk = std::max(8, std::min(256, std::atoi(e)));
   if (const char* e = std::getenv("FMMBEM_P2P_OCC")) c->p2p_occ = std::atoi(e);
   if (const char* e = std::getenv("FMMBEM_P2P_PLAIN")) c->p2p_scaled = std::atoi(e) ? 0 : 1;
+  if (const char* e = std::getenv("FMMBEM_P2P_CHUNK_CHG")) c->p2p_chunk_chg = std::max(8, std::min(256, std::atoi(e)));
   c->p2p_chunk = std::min(c->p2p_chunk, 128);  // <= 32 lanes x 4 targets per subset
+  c->p2p_chunk_chg = std::min(c->p2p_chunk_chg, 128);
   // near field concurrent with the far field: default on with several ranks (hides the exchange)
   c->overlap = opt.nranks > 1 ? 1 : 0;
   if (const char* e = std::getenv("FMMBEM_OVERLAP")) c->overlap = std::atoi(e);

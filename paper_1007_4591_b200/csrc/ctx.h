@@ -52,7 +52,7 @@ struct M2LWork {
 // P2P work items (leaf, first target, count) of one target set
 struct P2PItems {
   const PointSet* tgt = nullptr;
-  int leaf_lo = 0, leaf_hi = 0;
+  int leaf_lo = 0, leaf_hi = 0, chunk = 0;
   int64_t n = 0;
   DevBuf<int4> items;
 };
@@ -122,6 +122,7 @@ struct fmmbem_ctx {
   cudaEvent_t pev[33] = {};          // its chunk events (2 x 16 + 1)
   fmm::DevBuf<float> En, psi;       // charge fields (cached)
   bool have_fields = false;
+  bool fields_checked = false;       // the charge / panel-point coincidence check passed once
   fmm::DevBuf<int> flag;            // device error flags
   fmm::DevBuf<double> red;          // reduction scratch
 
@@ -135,11 +136,13 @@ struct fmmbem_ctx {
   std::vector<std::unique_ptr<fmm::P2PItems>> p2p_cache;
   int m2l_mode = 0;  // 0 = rotation O(P^3) when available, 1 = plain O(P^4)
   int p2p_chunk = 64;   // P2P targets per work item (FMMBEM_P2P_CHUNK)
+  int p2p_chunk_chg = 128; // ... of the charge-source near field (FMMBEM_P2P_CHUNK_CHG; 128 measured 2.6 vs 3.8 ms at C5)
   fmm::DevBuf<float4> p2p_src;  // scaled-form P2P sources of the current matvec (a y, a)
   fmm::DevBuf<unsigned> p2p_wmax;  // bits of max |w| the table was normalised by (power of two, P2P epilogue)
   int p2p_occ = 1;      // scaled K' P2P at 32 resident warps per SM (<= 64 registers; FMMBEM_P2P_OCC=0 -> 72)
   int p2p_scaled = 1;   // scaled-coordinate K' P2P (FMMBEM_P2P_PLAIN=1 -> plain form)
-  int64_t p2p_inter_kp = 0;  // exact P2P interaction count of the K' / A matvec
+  int64_t p2p_inter_kp = 0;   // exact P2P interaction count of the K' / A matvec
+  int64_t p2p_inter_chg = -1; // exact P2P interaction count of the charge-FMM (owned targets; -1 = not counted)
   int64_t m2l_pairs_kp = 0;
   // multi-GPU partition: this rank owns leaves [leaf_lo, leaf_hi); its panels are the
   // local points [pan_lo, pan_hi) of pan (the rest of pan is the near-field halo)
@@ -168,4 +171,5 @@ struct fmmbem_ctx {
   int overlap = 0;                             // 1: P2P concurrent with the upward/M2L/exchange chain
   bool timed_xg = false;
   bool timed_comm = false, timed_near = false;
+  bool timed_fields = false;  // the last timed evaluation was the charge-FMM
 };

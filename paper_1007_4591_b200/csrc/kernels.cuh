@@ -52,7 +52,7 @@ void halo_exchange(fmmbem_ctx* c, const float* x_owned, cudaStream_t st);
 const float4* prepare_p2p_sources(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
 void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o, bool self, bool check,
                 bool direct, cudaStream_t st);
-const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi);
+const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi, int chunk);
 
 // analytic near field (near.cu)
 void build_near(fmmbem_ctx* c, const double* V, const int* T, const double* cen, const double* nrm,
@@ -80,7 +80,8 @@ void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std
 void build_let(fmmbem_ctx* c, const std::vector<int64_t>& leaf_bounds, cudaStream_t s);
 void exchange_let(fmmbem_ctx* c, cudaStream_t s);
 // exact interaction count of launch_p2p(t, s) (list mode) -- setup-time helper
-int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct);
+int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct, int leaf_lo = 0,
+                  int leaf_hi = -1);
 
 // far field (expansions in c->Mx / c->Lx); l2p accumulates y += b far
 void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);

@@ -119,12 +119,13 @@ __device__ __forceinline__ void interact2s(const float4 s, float2 px, float2 py,
 
 template <int T, bool POT, bool DN, bool SELF, bool CHECK, bool SC = false, int MINB = 28>
 __global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
+  constexpr int TL = TILE;
   static_assert(!SC || (DN && !POT && !CHECK), "scaled form: normal derivative only");
-  __shared__ float4 tile[TILE];
-  __shared__ int own[SELF ? TILE : 1];
+  __shared__ float4 tile[TL];
+  __shared__ int own[SELF ? TL : 1];
   __shared__ int seg_src[MAXSEG], seg_cum[MAXSEG + 1];
   __shared__ float4 seg_sh[MAXSEG];
-  static_assert(4 * T * 32 * sizeof(float) <= sizeof(float4) * TILE, "split-K scratch aliases the tile");
+  static_assert(4 * T * 32 * sizeof(float) <= sizeof(float4) * TL, "split-K scratch aliases the tile");
   float(*red)[32] = reinterpret_cast<float(*)[32]>(tile);  // used only after the source loop
 
   const int4 it = a.items[blockIdx.x];
@@ -213,11 +214,11 @@ __global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
     shv = seg_sh[0];
   }
 
-  for (int base = 0; base < n_src; base += TILE) {
-    const int tcnt = min(TILE, n_src - base);
+  for (int base = 0; base < n_src; base += TL) {
+    const int tcnt = min(TL, n_src - base);
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < TILE / 32; ++q) {
+    for (int q = 0; q < TL / 32; ++q) {
       const int k = lane + 32 * q;
       if (k < tcnt) {
         const int v = base + k;
@@ -399,12 +400,12 @@ __global__ void k_scale_src(int64_t n, const float4* __restrict__ spos, const fl
   out[j] = r;
 }
 
-__global__ void k_count(int nl, const int* __restrict__ tbeg, const int* __restrict__ sbeg,
+__global__ void k_count(int nl, int lo, const int* __restrict__ tbeg, const int* __restrict__ sbeg,
                         const int* __restrict__ off, const int* __restrict__ idx, int direct, int ns,
                         unsigned long long* out) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int k = lo + blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long c = 0;
-  if (k < nl) {
+  if (k < lo + nl) {
     long long nt = tbeg[k + 1] - tbeg[k];
     long long s = 0;
     if (direct) s = ns;
@@ -433,16 +434,16 @@ __global__ void k_item_fill(int nl, const int* __restrict__ tbeg, int leaf0, int
 }  // namespace
 
 // (leaf, target chunk) work items of one target set, built once and cached
-const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi) {
+const P2PItems& p2p_items(fmmbem_ctx* c, const PointSet& t, int leaf_lo, int leaf_hi, int chunk) {
   for (auto& w : c->p2p_cache)
-    if (w->tgt == &t && w->leaf_lo == leaf_lo && w->leaf_hi == leaf_hi) return *w;
+    if (w->tgt == &t && w->leaf_lo == leaf_lo && w->leaf_hi == leaf_hi && w->chunk == chunk) return *w;
   const int nl = leaf_hi - leaf_lo;
-  const int chunk = c->p2p_chunk;
   cudaStream_t st = c->stream;
   auto w = std::make_unique<P2PItems>();
   w->tgt = &t;
   w->leaf_lo = leaf_lo;
   w->leaf_hi = leaf_hi;
+  w->chunk = chunk;
   DevBuf<int> cnt, pos;
   cnt.alloc(nl + 1);
   pos.alloc(nl + 1);
@@ -485,7 +486,8 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   const bool pot = o.pot.y != nullptr, dn = o.dn.y != nullptr;
   if (!pot && !dn) return;
   const P2PItems& items =
-      p2p_items(c, *t.set, t.leaf_lo, t.leaf_hi < 0 ? (int)c->tree.n_leaves : t.leaf_hi);
+      p2p_items(c, *t.set, t.leaf_lo, t.leaf_hi < 0 ? (int)c->tree.n_leaves : t.leaf_hi,
+                s.set == &c->chg ? c->p2p_chunk_chg : c->p2p_chunk);
   if (items.n == 0) return;
   P2PArgs a{};
   a.items = items.items.get();
@@ -524,20 +526,26 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   FMM_CHECK_LAUNCH();
 }
 
-int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct) {
+int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct, int leaf_lo,
+                  int leaf_hi) {
   const Tree& T = c->tree;
   DevBuf<unsigned long long> out;
   out.alloc(1);
   out.zero(c->stream);
-  int nl = (int)T.n_leaves;
-  k_count<<<ceil_div(nl, 256), 256, 0, c->stream>>>(nl, t.begin.get(), s.begin.get(), T.nbr_off.get(),
-                                                     T.nbr_idx.get(), direct ? 1 : 0, (int)s.n, out.get());
+  if (leaf_hi < 0) leaf_hi = (int)T.n_leaves;
+  const int nl = leaf_hi - leaf_lo;
+  if (nl > 0)
+    k_count<<<ceil_div(nl, 256), 256, 0, c->stream>>>(nl, leaf_lo, t.begin.get(), s.begin.get(), T.nbr_off.get(),
+                                                       T.nbr_idx.get(), direct ? 1 : 0, (int)s.n, out.get());
   FMM_CHECK_LAUNCH();
   unsigned long long h = 0;
+  int tb[2] = {0, 0};
   FMM_CUDA(cudaMemcpyAsync(&h, out.get(), sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  FMM_CUDA(cudaMemcpyAsync(&tb[0], t.begin.get() + leaf_lo, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  FMM_CUDA(cudaMemcpyAsync(&tb[1], t.begin.get() + leaf_hi, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   FMM_CUDA(cudaStreamSynchronize(c->stream));
   int64_t r = (int64_t)h;
-  if (self) r -= t.n * s.div;  // own-panel pairs are excluded (j != i)
+  if (self) r -= (int64_t)(tb[1] - tb[0]) * s.div;  // own-panel pairs are excluded (j != i)
   return r;
 }
 

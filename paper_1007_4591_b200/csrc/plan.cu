@@ -14,7 +14,9 @@
 // fmmbem_create copies its device skeleton to the host and calls plan_exchange; fmmbem_plan_create
 // (ABI, host only) builds the skeleton lists here first, so tests can check the plan on a CPU.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -161,24 +163,50 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
   X.let_send.assign(R, {});
   X.let_recv.assign(R, {});
   X.let_shared.clear();
-  std::vector<char> need(nc);
-  for (int p = 0; p < R; ++p) {
-    std::fill(need.begin(), need.end(), 0);
-    const int a = (int)X.leaf_bounds[p], b = (int)X.leaf_bounds[p + 1];
-    for (int64_t c = c0; c < nc; ++c) {
-      const int f = std::max(first[c], a), e = std::min(end[c], b);
-      if (e <= f || tpre[e] == tpre[f]) continue;  // no targets of p below c
-      for (int64_t k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k)
-        if (has_src[T.m2l_idx[k]]) need[T.m2l_idx[k]] = 1;
+  // one pass over the interaction lists: need[s] = ranks holding targets below some cell whose list
+  // contains s (a rank-bit mask; set-if-missing atomics, so the lists are split over host threads)
+  std::vector<std::atomic<unsigned long long>> need(nc);
+  for (auto& v : need) v.store(0, std::memory_order_relaxed);
+  auto work = [&](int64_t lo_c, int64_t hi_c) {
+    for (int64_t c = lo_c; c < hi_c; ++c) {
+      if (end[c] <= first[c]) continue;
+      unsigned long long tm = 0;
+      for (int p = lrank[first[c]]; p <= lrank[end[c] - 1]; ++p) {
+        const int f = std::max(first[c], (int)X.leaf_bounds[p]), e = std::min(end[c], (int)X.leaf_bounds[p + 1]);
+        if (e > f && tpre[e] > tpre[f]) tm |= 1ULL << p;
+      }
+      if (!tm) continue;
+      for (int64_t k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k) {
+        const int sidx = T.m2l_idx[k];
+        if (!has_src[sidx]) continue;
+        auto& v = need[sidx];
+        if ((v.load(std::memory_order_relaxed) & tm) != tm) v.fetch_or(tm, std::memory_order_relaxed);
+      }
     }
-    for (int64_t c = c0; c < nc; ++c) {
-      if (!need[c] || owner[c] < 0) continue;
-      if (p != me && owner[c] == me) X.let_send[p].push_back((int)c);
-      if (p == me && owner[c] != me) X.let_recv[owner[c]].push_back((int)c);
+  };
+  const int64_t ncell = nc - c0;
+  int nth = (int)std::max(1u, std::thread::hardware_concurrency() / (unsigned)std::max(1, R));
+  nth = (int)std::min<int64_t>(std::min(nth, 16), std::max<int64_t>(1, ncell / 65536));
+  if (nth <= 1) {
+    work(c0, nc);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nth; ++t) th.emplace_back(work, c0 + ncell * t / nth, c0 + ncell * (t + 1) / nth);
+    for (auto& t : th) t.join();
+  }
+  for (int64_t c = c0; c < nc; ++c) {
+    const unsigned long long m = need[c].load(std::memory_order_relaxed);
+    if (owner[c] < 0) {
+      if (has_src[c]) X.let_shared.push_back((int)c);
+      continue;
+    }
+    if (owner[c] == me) {
+      for (int p = 0; p < R; ++p)
+        if (p != me && (m >> p & 1ULL)) X.let_send[p].push_back((int)c);
+    } else if (m >> me & 1ULL) {
+      X.let_recv[owner[c]].push_back((int)c);
     }
   }
-  for (int64_t c = c0; c < nc; ++c)
-    if (owner[c] < 0 && has_src[c]) X.let_shared.push_back((int)c);
 }
 
 }  // namespace fmm
