@@ -241,7 +241,9 @@ enum {
   FMMBEM_PLAN_LET_SHARED = 4,  /* cells straddling ranks (peer ignored) */
   FMMBEM_PLAN_LEAF_BOUNDS = 5, /* nranks + 1 leaf bounds */
   FMMBEM_PLAN_CELL_KEYS = 6,   /* every cell's key, level-major */
-  FMMBEM_PLAN_LEVEL_OFFSETS = 7 /* level + 2 offsets into the cell numbering */
+  FMMBEM_PLAN_LEVEL_OFFSETS = 7, /* level + 2 offsets into the cell numbering */
+  FMMBEM_PLAN_NEIGHBOURS = 8,   /* `peer` = a leaf index: its neighbour leaves (incl. itself) */
+  FMMBEM_PLAN_INTERACTION = 9   /* `peer` = a cell index (level >= 2): its interaction list */
 };
 fmmbem_status fmmbem_plan_create(const uint64_t* leaf_keys, const int32_t* leaf_panels, const int32_t* leaf_charges,
                                  int64_t n_leaves, int32_t level, int32_t quad_points, int32_t nranks, int32_t rank,

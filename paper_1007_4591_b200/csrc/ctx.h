@@ -138,6 +138,7 @@ struct fmmbem_ctx {
   int p2p_chunk = 64;   // P2P targets per work item (FMMBEM_P2P_CHUNK)
   int p2p_chunk_chg = 128; // ... of the charge-source near field (FMMBEM_P2P_CHUNK_CHG; 128 measured 2.6 vs 3.8 ms at C5)
   fmm::DevBuf<float4> p2p_src;  // scaled-form P2P sources of the current matvec (a y, a)
+  fmm::DevBuf<int> p2p_counter;  // work-item counter of the persistent P2P launch
   fmm::DevBuf<unsigned> p2p_wmax;  // bits of max |w| the table was normalised by (power of two, P2P epilogue)
   int p2p_occ = 1;      // scaled K' P2P at 32 resident warps per SM (<= 64 registers; FMMBEM_P2P_OCC=0 -> 72)
   int p2p_scaled = 1;   // scaled-coordinate K' P2P (FMMBEM_P2P_PLAIN=1 -> plain form)

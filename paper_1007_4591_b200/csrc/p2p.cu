@@ -39,6 +39,8 @@ constexpr int MAXSEG = 32;
 
 struct P2PArgs {
   const int4* items;  // (leaf, first target, target count, 0)
+  int n_items;
+  int* counter;       // work-item counter of the persistent launch (zeroed before it)
   const float4* tpos;
   const float4* tnrm;
   const int* tbeg;
@@ -128,11 +130,21 @@ __global__ void __launch_bounds__(32, MINB) k_p2p(P2PArgs a) {
   static_assert(4 * T * 32 * sizeof(float) <= sizeof(float4) * TL, "split-K scratch aliases the tile");
   float(*red)[32] = reinterpret_cast<float(*)[32]>(tile);  // used only after the source loop
 
-  const int4 it = a.items[blockIdx.x];
-  const int leaf = it.x, tb = it.y, nt = it.z;
+  // persistent warps: a grid of (SMs x resident warps) one-warp blocks claims the work items in
+  // order from a global counter, so no warp slot waits for a block launch; every item is still
+  // computed whole by one warp (outputs written once, deterministic)
+  const int lane = threadIdx.x;
   int wexp = 0;
   if (SC) wexp = wmax_exp(*a.wmax);
-  const int lane = threadIdx.x;
+  int item;
+  {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(a.counter, 1);
+    item = __shfl_sync(0xffffffffu, v, 0);
+  }
+  for (; item < a.n_items;) {
+  const int4 it = a.items[item];
+  const int leaf = it.x, tb = it.y, nt = it.z;
   const int4 tc = a.ijk[leaf];
 
   // ---- source segments: neighbour leaves (self last) or, in direct mode, everything
@@ -346,6 +358,11 @@ P2P_UNROLL_LOOP(P2P_UNROLL)
       }
     }
   }
+  __syncwarp();  // shared memory of this item is free
+  int v = 0;
+  if (lane == 0) v = atomicAdd(a.counter, 1);
+  item = __shfl_sync(0xffffffffu, v, 0);
+  }
 }
 
 // T = 4 targets per lane: two packed FP32x2 pairs per shared-memory source load (a 64-register cap
@@ -491,6 +508,10 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   if (items.n == 0) return;
   P2PArgs a{};
   a.items = items.items.get();
+  a.n_items = (int)items.n;
+  if (c->p2p_counter.n < 1) c->p2p_counter.alloc(1);
+  FMM_CUDA(cudaMemsetAsync(c->p2p_counter.get(), 0, sizeof(int), st));
+  a.counter = c->p2p_counter.get();
   a.tpos = t.set->pos.get();
   a.tnrm = t.set->nrm.get();
   a.tbeg = t.set->begin.get();
@@ -509,7 +530,13 @@ void launch_p2p(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& 
   a.dn = o.dn;
   a.flag = c->flag.get();
   if (dn && !a.tnrm) throw Error(FMMBEM_E_INVALID, "normal derivative requested at targets without normals");
-  const int grid = (int)items.n;
+  static const int n_sm = [] {
+    int d = 0, v = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return v > 0 ? v : 148;
+  }();
+  const int grid = (int)std::min<int64_t>(items.n, (int64_t)n_sm * 32);  // 32 one-warp blocks per SM
   const bool sc = c->p2p_scaled != 0 && dn && !pot && !check;
   if (sc) {
     a.ssc = s.scaled;

@@ -257,6 +257,17 @@ int64_t fmmbem_plan_list(const fmmbem_plan* p, int32_t list, int32_t peer, int64
   };
   const bool per_peer = list >= FMMBEM_PLAN_HALO_SEND && list <= FMMBEM_PLAN_LET_RECV;
   if (per_peer && (peer < 0 || peer >= R)) return -1;
+  const int64_t nl = T.lvl_off[T.L + 1] - T.lvl_off[T.L], nc = T.lvl_off[T.L + 1];
+  if (list == FMMBEM_PLAN_NEIGHBOURS) {
+    if (peer < 0 || peer >= nl) return -1;
+    std::vector<int> v(T.nbr_idx.begin() + T.nbr_off[peer], T.nbr_idx.begin() + T.nbr_off[peer + 1]);
+    return emit(v);
+  }
+  if (list == FMMBEM_PLAN_INTERACTION) {
+    if (peer < 0 || peer >= nc) return -1;
+    std::vector<int> v(T.m2l_idx.begin() + T.m2l_off[peer], T.m2l_idx.begin() + T.m2l_off[peer + 1]);
+    return emit(v);
+  }
   switch (list) {
     case FMMBEM_PLAN_HALO_SEND: return emit(X.halo_send[peer]);
     case FMMBEM_PLAN_HALO_RECV: return emit(X.halo_recv[peer]);

@@ -111,3 +111,39 @@ def test_nonfinite_vertex_rejected():
     v[3, 1] = np.nan
     with pytest.raises(FmmbemError, match="E_INVALID.*non-finite"):
         solver(dict(cfg, vertices=v))
+
+
+def test_device_tree_lists_equal_host_plan_lists():
+    """The device tree (tree.cu kernels) and the host skeleton of fmmbem_plan (plan.cu, pinned by the
+    dual-accounting brute force in tests/test_multigpu_host.py) have the same neighbour and
+    interaction lists: same leaf keys from the library's root cube, same list sizes."""
+    import ctypes as C
+    from paper_1007_4591_b200 import _lib
+    cfg = configs.lysozyme(nu=30, n_atoms=300)
+    s = solver(cfg, terms=13, leaf_points=32)
+    info = s.tree_info()
+    L, W, x0 = info["levels"], info["root_width"], np.array(info["root_origin"])
+    v, t = cfg["vertices"], cfg["triangles"]
+    cen = (v[t[:, 0]] + v[t[:, 1]] + v[t[:, 2]]) / 3.0
+
+    def keys_of(p):
+        g = np.clip(np.floor((p - x0) * (2 ** 21 / W)), 0, 2 ** 21 - 1).astype(np.int64) >> (21 - L)
+        k = np.zeros(len(p), np.uint64)
+        for b in range(L):
+            for d in range(3):
+                k |= ((g[:, d].astype(np.uint64) >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + d)
+        return k
+    kp, kc = keys_of(cen), keys_of(cfg["charge_xyz"])
+    keys = np.unique(np.concatenate([kp, kc]))
+    assert len(keys) == info["n_leaves"]
+    npan = (np.searchsorted(np.sort(kp), keys, "right") - np.searchsorted(np.sort(kp), keys, "left")).astype(np.int32)
+    nchg = (np.searchsorted(np.sort(kc), keys, "right") - np.searchsorted(np.sort(kc), keys, "left")).astype(np.int32)
+    lib = _lib.load()
+    h = C.c_void_p()
+    assert lib.fmmbem_plan_create(keys.ctypes.data_as(C.POINTER(C.c_uint64)), npan.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  nchg.ctypes.data_as(C.POINTER(C.c_int32)), len(keys), L, 1, 1, 0, C.byref(h)) == 0
+    n_cells = lib.fmmbem_plan_list(h, 6, 0, None)
+    nbr = sum(lib.fmmbem_plan_list(h, 8, k, None) for k in range(len(keys)))
+    m2l = sum(lib.fmmbem_plan_list(h, 9, c, None) for c in range(n_cells))
+    lib.fmmbem_plan_destroy(h)
+    assert (n_cells, nbr, m2l) == (info["n_cells"], info["nbr_pairs"], info["m2l_pairs"])

@@ -215,3 +215,45 @@ def test_exchange_plan_brute_force_over_gloo(world):
     keys, npan, nchg, L = real_skeleton()
     assert L >= 3 and len(keys) > 50
     brute_force_check(plans, keys, npan, nchg, L)
+
+
+def test_tree_lists_dual_accounting():
+    """SPEC S:164 / S:173 dual accounting, brute force on the library's host lists (plan.cu, the same
+    definitions as tree.cu's kernels): for every leaf t, its neighbour leaves plus the leaves below
+    every cell in the interaction lists of t and of each of its ancestors cover ALL leaves exactly
+    once -- every source is counted once, by P2P or by exactly one M2L."""
+    import ctypes as C
+    from paper_1007_4591_b200 import _lib
+    keys, npan, nchg, L = real_skeleton()
+    lib = _lib.load()
+    k = np.ascontiguousarray(keys, np.uint64)
+    h = C.c_void_p()
+    assert lib.fmmbem_plan_create(k.ctypes.data_as(C.POINTER(C.c_uint64)), npan.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  nchg.ctypes.data_as(C.POINTER(C.c_int32)), len(k), L, 1, 1, 0, C.byref(h)) == 0
+
+    def lst(kind, peer):
+        n = lib.fmmbem_plan_list(h, kind, peer, None)
+        out = np.empty(max(n, 1), np.int64)
+        lib.fmmbem_plan_list(h, kind, peer, out.ctypes.data_as(C.POINTER(C.c_int64)))
+        return out[:n]
+
+    off = lst(7, 0)
+    ck = lst(6, 0).astype(np.uint64)
+    nl = len(keys)
+    leaf_keys = np.asarray(keys, np.uint64)
+    ijk = np.stack(_demorton(leaf_keys), 1)
+    for t in range(nl):
+        count = np.zeros(nl, np.int64)
+        nb = lst(8, t)
+        # neighbours: exactly the leaves with max |d ijk| <= 1 (brute force), incl. t itself
+        want = np.nonzero(np.abs(ijk - ijk[t]).max(1) <= 1)[0]
+        assert sorted(nb.tolist()) == want.tolist()
+        count[nb] += 1
+        for l in range(2, L + 1):  # ancestor of t at level l and its interaction list
+            a = int(np.searchsorted(ck[off[l]:off[l + 1]], leaf_keys[t] >> np.uint64(3 * (L - l)))) + off[l]
+            for s in lst(9, a):
+                ls_ = int(np.searchsorted(np.asarray(off), s, "right")) - 1
+                below = (leaf_keys >> np.uint64(3 * (L - ls_))) == ck[s]
+                count[below] += 1
+        assert count.min() == 1 and count.max() == 1, (t, np.nonzero(count != 1)[0][:10])
+    lib.fmmbem_plan_destroy(h)
