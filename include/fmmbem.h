@@ -133,7 +133,9 @@ fmmbem_status fmmbem_local_panel_ids(const fmmbem_ctx* ctx, int64_t* global_ids_
 typedef enum {
   FMMBEM_OP_KPRIME = 0, /* y_i = sum_{j!=i} A_j x_j sum_g w_g dG/dn_i(c_i, y_jg)   (Eq. 4 operator) */
   FMMBEM_OP_SINGLE = 1, /* y_i = sum_{j!=i} A_j x_j sum_g w_g G(c_i, y_jg)         (Eq. 5, 1/r)     */
-  FMMBEM_OP_A = 2       /* y = x - f * KPRIME(x), f = 2(eps_II-eps_I)/(eps_I+eps_II) (GMRES operator, A1) */
+  FMMBEM_OP_A = 2,      /* y = x - f * KPRIME(x), f = 2(eps_II-eps_I)/(eps_I+eps_II) (GMRES operator, A1) */
+  FMMBEM_OP_DOUBLE = 3  /* y_i = sum_{j!=i} A_j x_j sum_g w_g dG/dn_y(c_i, y_jg), n_y = n_j: the double layer K,
+                           adjoint of KPRIME (dipole sources; not with near_mode) */
 } fmmbem_op;
 
 /* One FMM matrix-vector product.  x_dev, y_dev: caller-owned device

@@ -35,6 +35,8 @@ def lib():
         L.oracle_dn_sum.restype = ctypes.c_int
         L.oracle_pot_sum.argtypes = [ctypes.c_int64, d, i, ctypes.c_int64, d, d, i, d]
         L.oracle_pot_sum.restype = ctypes.c_int
+        L.oracle_dipole_sum.argtypes = [ctypes.c_int64, d, i, ctypes.c_int64, d, d, d, i, d]
+        L.oracle_dipole_sum.restype = ctypes.c_int
         L.oracle_threads.restype = ctypes.c_int
         L.oracle_tri_integrals.argtypes = [ctypes.c_int64, d, d, d, ctypes.POINTER(ctypes.c_int32), d, d]
         L.oracle_tri_integrals.restype = None
@@ -62,6 +64,20 @@ def dn_sum(x, n, tid, y, w, owner):
     out = np.zeros(len(x))
     bad = lib().oracle_dn_sum(len(x), _dp(x), _dp(n), _ip(tid), len(y), _dp(y), _dp(w),
                               _ip(owner), _dp(out))
+    if bad:
+        raise ValueError("coincident target/source pair (SURVEY A14)")
+    return out
+
+
+def dipole_sum(x, tid, y, m, w, owner):
+    """out[i] = sum_j w[j] m_j . (x_i - y_j) / (4 pi |x_i - y_j|^3)  (source-normal derivative of G)."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64); m = np.ascontiguousarray(m, np.float64)
+    w = np.ascontiguousarray(w, np.float64)
+    tid = None if tid is None else np.ascontiguousarray(tid, np.int64)
+    owner = None if owner is None else np.ascontiguousarray(owner, np.int64)
+    out = np.zeros(len(x))
+    bad = lib().oracle_dipole_sum(len(x), _dp(x), _ip(tid), len(y), _dp(y), _dp(m), _dp(w), _ip(owner), _dp(out))
     if bad:
         raise ValueError("coincident target/source pair (SURVEY A14)")
     return out

@@ -178,6 +178,16 @@ class SingleRows(KprimeRows):
         return _cdirect.pot_sum(self.pan.centroid[idx], idx, self.y, self.w, self.owner)
 
 
+def apply_double(pan: Panels, x, rows=None):
+    """Double layer: (Kx)_i = sum_{j!=i} x_j A_j sum_g w_g dG/dn_y(c_i, y_jg), n_y = n_j --
+    the continuum adjoint of K' (Eq. 4, P:326 uses K'); K_ii = 0 for a flat panel (c_i lies in its plane)."""
+    y, owner, aw = pan.sources()
+    w = np.repeat(np.asarray(x, np.float64), pan.K) * aw
+    m = np.repeat(pan.normal, pan.K, axis=0)
+    idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)
+    return _cdirect.dipole_sum(pan.centroid[idx], idx, y, m, w, owner)
+
+
 def apply_single(pan: Panels, x, rows=None):
     """O5: (Vx)_i = sum_{j!=i} x_j A_j sum_g w_g G(c_i, y_jg)  (Eq. 5)."""
     idx = np.arange(pan.n, dtype=np.int64) if rows is None else np.asarray(rows, np.int64)

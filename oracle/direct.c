@@ -6,6 +6,7 @@
  *
  *   G(x, y)          = 1 / (4 pi |x - y|)                         (Eq. 5)
  *   dG/dn_x (x, y)   = -n_x . (x - y) / (4 pi |x - y|^3)           (Eq. 4)
+ *   dG/dn_y (x, y)   =  n_y . (x - y) / (4 pi |x - y|^3)           (double layer)
  *
  * Pair (i, j) is skipped when tid[i] == owner[j] (both non-NULL): this is the
  * "j != i" of the discrete operators K' and V (SPEC.md
@@ -44,6 +45,27 @@ int oracle_dn_sum(int64_t nt, const double* x, const double* n, const int64_t* t
       double r = sqrt(r2);
       double ndot = n[3 * i] * dx + n[3 * i + 1] * dy + n[3 * i + 2] * dz;
       s += w[j] * (-ndot / (FOUR_PI * r2 * r));
+    }
+    out[i] = s;
+  }
+  return bad;
+}
+
+/* out[i] = sum_j w[j] * dG/dn_y(x_i, y_j) with the SOURCE normal m_j (double-layer kernel) */
+int oracle_dipole_sum(int64_t nt, const double* x, const int64_t* tid, int64_t ns, const double* y,
+                      const double* m, const double* w, const int64_t* owner, double* out) {
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(| : bad)
+  for (int64_t i = 0; i < nt; ++i) {
+    double s = 0.0;
+    for (int64_t j = 0; j < ns; ++j) {
+      if (tid && owner && tid[i] == owner[j]) continue;
+      double dx = x[3 * i] - y[3 * j], dy = x[3 * i + 1] - y[3 * j + 1], dz = x[3 * i + 2] - y[3 * j + 2];
+      double r2 = dx * dx + dy * dy + dz * dz;
+      if (r2 == 0.0) { bad = 1; continue; }
+      double r = sqrt(r2);
+      double mdot = m[3 * j] * dx + m[3 * j + 1] * dy + m[3 * j + 2] * dz;
+      s += w[j] * (mdot / (FOUR_PI * r2 * r));
     }
     out[i] = s;
   }

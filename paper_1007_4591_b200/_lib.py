@@ -15,7 +15,7 @@ OK, NOT_CONVERGED = 0, 1
 E_INVALID, E_DEGENERATE, E_COINCIDENT, E_CUDA, E_NOMEM, E_NCCL = -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "E_INVALID", -2: "E_DEGENERATE", -3: "E_COINCIDENT",
                 -4: "E_CUDA", -5: "E_NOMEM", -6: "E_NCCL"}
-OP_KPRIME, OP_SINGLE, OP_A = 0, 1, 2
+OP_KPRIME, OP_SINGLE, OP_A, OP_DOUBLE = 0, 1, 2, 3
 BIBEE_CFA, BIBEE_P, BIBEE_LB = 0, 1, 2
 
 

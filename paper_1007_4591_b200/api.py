@@ -13,7 +13,7 @@ import numpy as np
 from . import _lib as L
 
 BIBEE = {"cfa": L.BIBEE_CFA, "p": L.BIBEE_P, "lb": L.BIBEE_LB}
-OPS = {"kprime": L.OP_KPRIME, "single": L.OP_SINGLE, "A": L.OP_A}
+OPS = {"kprime": L.OP_KPRIME, "single": L.OP_SINGLE, "A": L.OP_A, "double": L.OP_DOUBLE}
 
 
 def _dp(a):

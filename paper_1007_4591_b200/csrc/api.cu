@@ -269,7 +269,8 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     rec(E_UP0, fs);
     const SrcArg& sf = s;
     c->Mx.zero(fs);  // the upward sweep, split for the phase events: P2M, then M2M level by level
-    launch_p2m_range(c, sf, sf.leaf_lo, sf.leaf_hi < 0 ? (int)c->tree.n_leaves : sf.leaf_hi, fs);
+    if (sf.dipole) launch_p2m_dipole(c, sf, sf.leaf_lo, sf.leaf_hi < 0 ? (int)c->tree.n_leaves : sf.leaf_hi, fs);
+    else launch_p2m_range(c, sf, sf.leaf_lo, sf.leaf_hi < 0 ? (int)c->tree.n_leaves : sf.leaf_hi, fs);
     rec(E_P2M1, fs);
     launch_m2m_levels(c, sf, fs);
     rec(E_UP1, fs);
@@ -298,7 +299,8 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     rec(E_XG1, st);
   }
   rec(E_P2P0, st);
-  launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
+  if (s.dipole) launch_p2p_dipole(c, t, s, o.pot.y, o.pot.b, c->opt.direct != 0 || c->tree.L < 2, st);
+  else launch_p2p(c, t, s, o, self, check, c->opt.direct != 0, st);
   rec(E_P2P1, st);
   if (ovl) FMM_CUDA(cudaStreamWaitEvent(st, c->join, 0));
   rec(E_L2P0, st);
@@ -317,7 +319,7 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
 // global tree indices land in the slice)
 Outputs op_outputs(fmmbem_ctx* c, fmmbem_op op, const float* xg, float* yg) {
   Outputs o;
-  if (op == FMMBEM_OP_SINGLE) {
+  if (op == FMMBEM_OP_SINGLE || op == FMMBEM_OP_DOUBLE) {
     o.pot.y = yg;
     o.pot.b = (float)(1.0 / FOUR_PI);
   } else {
@@ -345,9 +347,10 @@ void apply_op(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, cudaStream_
   bool dist = false;
   if (timing) cudaEventRecord(c->ev[E_AG0], st);
   SrcArg s = kp_src(c, x, st, &dist);
+  s.dipole = (op == FMMBEM_OP_DOUBLE);
   if (timing) cudaEventRecord(c->ev[E_AG1], st);
   fmm_eval(c, t, s, o, /*self=*/true, /*check=*/false, st, timing, dist);
-  if (c->opt.near_mode) {  // analytic near-field correction (a11): y += b C x over full x
+  if (c->opt.near_mode && op != FMMBEM_OP_DOUBLE) {  // analytic near-field correction (a11): y += b C x
     const bool single = (op == FMMBEM_OP_SINGLE);
     const float b = (op == FMMBEM_OP_A) ? (float)(-c->f) : 1.f;
     apply_near(c, single, s.x, yg, b, st);
@@ -803,7 +806,9 @@ fmmbem_status fmmbem_split_costs(const double* costs, int64_t n, int32_t parts, 
 fmmbem_status fmmbem_matvec(fmmbem_ctx* c, fmmbem_op op, const float* x, float* y, void* stream) {
   API_BEGIN
   if (!c || !x || !y || x == y) throw Error(FMMBEM_E_INVALID, "matvec: null or aliased vectors");
-  if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_A) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
+  if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_DOUBLE) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
+  if (op == FMMBEM_OP_DOUBLE && c->opt.near_mode)
+    throw Error(FMMBEM_E_INVALID, "matvec: the double layer has no analytic near-field option");
   DevGuard dg(c->device);
   cudaStream_t st = (cudaStream_t)stream;
   order_after_last(c, st);
@@ -896,7 +901,9 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
 fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* yh) {
   API_BEGIN
   if (!c || !xh || !yh) throw Error(FMMBEM_E_INVALID, "matvec_host: null vectors");
-  if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_A) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
+  if (op < FMMBEM_OP_KPRIME || op > FMMBEM_OP_DOUBLE) throw Error(FMMBEM_E_INVALID, "matvec: bad op");
+  if (op == FMMBEM_OP_DOUBLE && c->opt.near_mode)
+    throw Error(FMMBEM_E_INVALID, "matvec: the double layer has no analytic near-field option");
   DevGuard dg(c->device);
   cudaStream_t st = c->stream;
   order_after_last(c, st);
@@ -904,7 +911,7 @@ fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, f
   c->tmp_x.alloc(std::max<int64_t>(n, 1));
   c->tmp_y.alloc(std::max<int64_t>(n, 1));
   const bool pipelined = c->nranks == 1 && c->K == 1 && c->opt.near_mode == 0 && c->opt.direct == 0 &&
-                         c->tree.L >= 2 && std::getenv("FMMBEM_E2E_PLAIN") == nullptr;
+                         c->tree.L >= 2 && op != FMMBEM_OP_DOUBLE && std::getenv("FMMBEM_E2E_PLAIN") == nullptr;
   if (pipelined) {
     matvec_host_pipelined(c, op, xh, yh);
     mark_done(c, st);

@@ -24,6 +24,7 @@ struct SrcArg {
   const PointSet* set = nullptr;
   const float* x = nullptr;
   const float* halo_src = nullptr;  // nranks > 1: owned weights whose halo exchange fmm_eval runs before P2P
+  bool dipole = false;  // double layer: sources are dipoles of moment w n (pan.nrm of the source's panel)
   const float4* scaled = nullptr;  // prepared scaled-form P2P sources (prepare_p2p_sources), else built in launch_p2p
   int leaf_lo = 0, leaf_hi = -1;
   const int* cnt = nullptr;
@@ -92,6 +93,11 @@ void launch_m2l(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStrea
 void launch_downward(fmmbem_ctx* c, const int* tgt_cnt, cudaStream_t st);
 void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t st);
 void init_tables(fmmbem_ctx* c);
+
+// double-layer operator (dipole.cu): P2M of dipole sources over leaves [lo, hi), near field y = b sum
+void launch_p2m_dipole(fmmbem_ctx* c, const SrcArg& s, int lo, int hi, cudaStream_t st);
+void launch_p2p_dipole(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, float* y, float b, bool direct,
+                       cudaStream_t st);
 
 // order-specialised P2M / L2P (expansions.cu)
 bool exp_specialised(int P);

@@ -1113,8 +1113,7 @@ void build_halo(fmmbem_ctx* c, const std::vector<int>& hgb, DevBuf<float4>& opos
   }
   // static exchange: positions (+ quadrature points) and global ids of the halo panels
   P.pos.alloc(std::max<int64_t>(nloc, 1));
-  P.nrm.alloc(std::max<int64_t>(nloc, 1));
-  P.nrm.zero(s);  // halo panels are sources only
+  P.nrm.alloc(std::max<int64_t>(nloc, 1));  // halo normals: the double layer's dipole sources
   if (n_own) {
     FMM_CUDA(cudaMemcpyAsync(P.pos.get() + c->pan_lo, opos.get(), n_own * sizeof(float4), cudaMemcpyDeviceToDevice, s));
     FMM_CUDA(cudaMemcpyAsync(P.nrm.get() + c->pan_lo, onrm.get(), n_own * sizeof(float4), cudaMemcpyDeviceToDevice, s));
@@ -1132,13 +1131,15 @@ void build_halo(fmmbem_ctx* c, const std::vector<int>& hgb, DevBuf<float4>& opos
   }
   {
     const int64_t ns = std::max<int64_t>(H.sent, 1);
-    DevBuf<float4> spos, squad;
+    DevBuf<float4> spos, snrm, squad;
     DevBuf<long long> sgid;
     spos.alloc(ns);
+    snrm.alloc(ns);
     sgid.alloc(ns);
     if (K > 1) squad.alloc(ns * K);
     if (H.sent) {
       k_gather_f4<<<ceil_div(H.sent, TB), TB, 0, s>>>(H.sent, H.sidx.get(), opos.get(), spos.get());
+      k_gather_f4<<<ceil_div(H.sent, TB), TB, 0, s>>>(H.sent, H.sidx.get(), onrm.get(), snrm.get());
       k_gather_i64<<<ceil_div(H.sent, TB), TB, 0, s>>>(H.sent, H.sidx.get(), ogid.get(), sgid.get());
       if (K > 1) k_gather_f4_quad<<<ceil_div(H.sent * K, TB), TB, 0, s>>>(H.sent, K, H.sidx.get(), oquad.get(), squad.get());
       FMM_CHECK_LAUNCH();
@@ -1158,6 +1159,7 @@ void build_halo(fmmbem_ctx* c, const std::vector<int>& hgb, DevBuf<float4>& opos
       comm_alltoallv_bytes(c, sp, sn, rp, rn, s);
     };
     xchg(spos.get(), P.pos.get(), sizeof(float4));
+    xchg(snrm.get(), P.nrm.get(), sizeof(float4));
     xchg(sgid.get(), lgid.get(), sizeof(long long));
     if (K > 1) xchg(squad.get(), lquad.get(), K * sizeof(float4));
     FMM_CUDA(cudaStreamSynchronize(s));

@@ -33,6 +33,7 @@ def test_two_gpus_match_one(case):
             m = rk[mode]
             assert m["n_local"] > 0
             assert m["matvec_rel"] < 1e-6, m
+            assert m["double_rel"] < 1e-6, m
             assert m["host_rel"] == 0.0, m  # host-buffer product = device product (same path on N > 1)
             g, o, gi, oi = m["solve"]
             assert abs(g / o - 1) < 1e-6 and abs(gi - oi) <= 1, m

@@ -287,3 +287,40 @@ def test_host_buffer_matvec_equals_device_matvec(problems, op):
     yp = torch.empty_like(xp).pin_memory()
     yh = s.matvec_host(xp.numpy(), op, y_host=yp.numpy())
     assert bem.rel_l2(yh.astype(np.float64), yd.astype(np.float64)) < 1e-6
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_double_layer_matches_oracle(problems, case):
+    """Option FMMBEM_OP_DOUBLE: the double-layer K with dipole sources -- all-pairs
+    (FP32 sums) and FMM (dipole P2M + the same M2M/M2L/L2L/L2P) against the oracle's direct sums, for
+    random x and x = 1 (K 1 -> -1/2, Gauss)."""
+    cfg, P = problems[case]
+    for x in (np.random.default_rng(12).normal(size=P.pan.n), np.ones(P.pan.n)):
+        ref = bem.apply_double(P.pan, x)
+        for kw, tol in ((dict(direct=1), 2e-5), (dict(terms=13, leaf_points=16), 1e-4)):
+            err = bem.rel_l2(run(solver(cfg, **kw), x, "double"), ref)
+            assert err < tol, (kw, err)
+
+
+def test_double_layer_is_the_adjoint_of_kprime_on_the_gpu(problems):
+    """sum_i A_i v_i (K'u)_i = sum_j A_j u_j (K v)_j (exact for the centroid rule), both sides from
+    the GPU FMM products: equal to the FMM accuracy."""
+    cfg, P = problems["lyso20"]
+    s = solver(cfg, terms=13, leaf_points=16)
+    rng = np.random.default_rng(13)
+    u, v = rng.normal(size=P.pan.n), rng.normal(size=P.pan.n)
+    a = P.pan.area
+    lhs = np.sum(a * v * run(s, u, "kprime"))
+    rhs = np.sum(a * u * run(s, v, "double"))
+    scale = np.sqrt(np.sum(a * v * v) * np.sum(a * run(s, u, "kprime") ** 2))
+    assert abs(lhs - rhs) < 1e-4 * scale
+
+
+def test_double_layer_quadrature_rule():
+    cfg = configs.kirkwood(10)
+    P = bem.Problem(cfg, K=3)
+    x = np.random.default_rng(14).normal(size=P.pan.n)
+    ref = bem.apply_double(P.pan, x)
+    for direct, tol in ((1, 2e-5), (0, 1e-4)):
+        s = solver(cfg, quad_points=3, direct=direct, terms=13, leaf_points=16)
+        assert bem.rel_l2(run(s, x, "double"), ref) < tol

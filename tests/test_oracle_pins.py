@@ -450,3 +450,26 @@ def test_rows_helpers_equal_full_operators():
     assert np.array_equal(bem.SingleRows(p, x)(rows), bem.apply_single(p, x)[rows])
     En = bem.normal_field(p, cfg["charge_xyz"], cfg["charge_q"], 4.0)
     assert np.array_equal(bem.normal_field(p, cfg["charge_xyz"], cfg["charge_q"], 4.0, rows=rows), En[rows])
+
+
+def test_double_layer_adjoint_of_kprime_and_gauss_limit():
+    """Double layer K: with the centroid rule the discrete K is exactly the
+    area-weighted adjoint of the (pinned) discrete K': sum_i A_i v_i (K'u)_i = sum_j A_j u_j (K v)_j;
+    and Gauss's integral of the double-layer kernel over a closed surface seen from a surface point
+    is -1/2 (principal value), so K 1 -> -1/2 on spheres, first order in the panel size."""
+    devs = []
+    for nu in (8, 16, 32):
+        cfg = configs.born(nu, radius=1.5)
+        p = bem.Panels(cfg["vertices"], cfg["triangles"])
+        rng = np.random.default_rng(nu)
+        u, v = rng.normal(size=p.n), rng.normal(size=p.n)
+        lhs = np.sum(p.area * v * bem.apply_kprime(p, u))
+        rhs = np.sum(p.area * u * bem.apply_double(p, v))
+        assert abs(lhs - rhs) <= 1e-12 * np.sum(p.area * np.abs(v) * np.abs(bem.apply_kprime(p, np.abs(u))))
+        devs.append(np.abs(bem.apply_double(p, np.ones(p.n)) + 0.5).max())
+    assert devs[0] > devs[1] > devs[2] and devs[2] < 0.01, devs
+    assert 1.6 < devs[1] / devs[2] < 2.5  # O(h)
+    # a 3-point rule approaches the same limit
+    cfg = configs.born(16)
+    p3 = bem.Panels(cfg["vertices"], cfg["triangles"], K=3)
+    assert abs(np.mean(bem.apply_double(p3, np.ones(p3.n))) + 0.5) < 0.02

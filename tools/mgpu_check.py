@@ -55,6 +55,7 @@ def main():
     s1 = Solver.from_config(cfg, **opts)
     dev = lambda s, v: torch.tensor(v[s.local_ids], dtype=torch.float32, device="cuda")
     y1 = s1.to_global(s1.matvec(dev(s1, x), "kprime").cpu().numpy())
+    yd1 = s1.to_global(s1.matvec(dev(s1, x), "double").cpu().numpy())
     r1 = s1.solve()
     b1 = s1.bibee("cfa")
     phi1 = s1.reaction_potential(r1["sigma"])
@@ -62,12 +63,13 @@ def main():
         c = cfg if mode == 0 else part_of(cfg, rank, world)
         s = Solver.distributed(c, input_mode=mode, **opts)
         y = gather(s, s.matvec(dev(s, x), "kprime"))
+        yd = gather(s, s.matvec(dev(s, x), "double"))  # dipole sources: the halo carries normals
         yh = s.matvec_host(x[s.local_ids].astype(np.float32), "kprime")
         r = s.solve()
         b = s.bibee("cfa")
         sig = gather(s, r["sigma"])
         phi = s.reaction_potential(torch.tensor(sig[s.local_ids], dtype=torch.float32, device="cuda"))
-        res[f"mode{mode}"] = dict(n_local=s.n, matvec_rel=rel(y, y1),
+        res[f"mode{mode}"] = dict(n_local=s.n, matvec_rel=rel(y, y1), double_rel=rel(yd, yd1),
                                   host_rel=float(np.abs(yh - y[s.local_ids]).max()),
                                   solve=(r["dG"], r1["dG"], r["iterations"], r1["iterations"]),
                                   bibee=(b["dG"], b1["dG"]), phi_rel=rel(phi, phi1))
