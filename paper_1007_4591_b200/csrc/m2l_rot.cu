@@ -775,16 +775,19 @@ void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st) {
   FMM_CHECK_LAUNCH();
 }
 
+#ifndef M2L_RPW
+#define M2L_RPW 16  // rows per warp in a CTA's Morton window
+#endif
 template <int P, int W>
 void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem, cudaStream_t st) {
   static unsigned long long attr_devices = 0;  // the attribute is per device: set it once on each
   int dev = 0;
   FMM_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !(attr_devices >> dev & 1ULL)) {
-    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W, M2L_RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_devices |= 1ULL << dev;
   }
-  k_m2l_rot_sync<P, W, 16><<<ceil_div(w.rows, 16 * W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
+  k_m2l_rot_sync<P, W, M2L_RPW><<<ceil_div(w.rows, M2L_RPW * W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
                                                                    w.idx.get(), T.key.get(), c->Mx.get(),
                                                                    c->Lx.get());
 }
