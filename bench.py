@@ -249,6 +249,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1024, help="oracle sample rows for cpu_baseline/parity")
     ap.add_argument("--bibee-calls", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--near-mode", type=int, default=0, help="1: analytic flat-panel near field (option a11)")
     args = ap.parse_args()
     if args.terms is None:
         args.terms = 10 if args.config == "cube" else DEFAULT_TERMS  # the paper's control is P = 10
@@ -274,9 +275,10 @@ def main():
     t0 = time.perf_counter()
     if world > 1:  # octree domain decomposition over NCCL
         s = Solver.distributed(cfg, input_mode=1 if parts else 0, terms=args.terms, leaf_points=args.leaf_points,
-                               device=local)
+                               device=local, near_mode=args.near_mode)
     else:
-        s = Solver.from_config(cfg, terms=args.terms, leaf_points=args.leaf_points, device=local)
+        s = Solver.from_config(cfg, terms=args.terms, leaf_points=args.leaf_points, device=local,
+                               near_mode=args.near_mode)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     info = s.tree_info()
@@ -305,7 +307,7 @@ def main():
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
-    keys = ("upward", "p2m", "m2m", "comm", "m2l", "p2p", "l2p", "l2l", "leaf_l2p", "total")
+    keys = ("upward", "p2m", "m2m", "comm", "m2l", "p2p", "l2p", "l2l", "leaf_l2p", "near", "total")
     phases = {k: [] for k in keys}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -426,7 +428,7 @@ def main():
            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": wname, "n_panels": n, "n_charges": len(cfg["charge_q"]), "terms": P,
                       "input": "each rank builds its block of copies (input_mode 1)" if parts else "full mesh",
-                      "quad_points": 1, "leaf_points": args.leaf_points,
+                      "quad_points": 1, "leaf_points": args.leaf_points, "near_mode": args.near_mode,
                       "operator": "V (potential)" if cube else "A = I - f K'",
                       "tree_levels": info["levels"], "n_leaves": info["n_leaves"],
                       "l2_flush": "inputs larger than L2 (x 409 MB, points 3.3 GB)",

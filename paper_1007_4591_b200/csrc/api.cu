@@ -738,6 +738,12 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
     if (rot_supported(c->P) && c->m2l_mode == 0) c->m2l_pairs_kp = m2l_work(c, src.cell_cnt.get(), tc, s).pairs;
     else c->m2l_pairs_kp = c->tree.m2l_pairs;
   }
+  // everything a matvec allocates or builds lazily is prepared here: no allocation (an implicit
+  // device synchronisation) can then fall between the concurrent NCCL exchanges of a matvec
+  p2p_items(c, c->pan, c->leaf_lo, c->leaf_hi, c->p2p_chunk);
+  c->p2p_src.alloc(std::max<int64_t>(src.n, 1));
+  c->p2p_wmax.alloc(1);
+  c->p2p_counter.alloc(1);
   FMM_CUDA(cudaStreamSynchronize(s));
   *out = c;
   return FMMBEM_OK;

@@ -1,7 +1,8 @@
 """Multi-GPU parity: the octree domain decomposition over NCCL -- halo exchange of the
 near-field weights, LET multipoles -- reproduces the single-GPU matvec, GMRES solve, BIBEE energy and
 reaction potential, with the full mesh on every rank (input_mode 0) and with every rank passing only
-its part (input_mode 1), and with the self-term / analytic near-field options.  Needs >= 2 GPUs."""
+its part (input_mode 1; also with every triangle on one rank and none on the others), and with the
+self-term / analytic near-field options.  Needs >= 2 GPUs."""
 import json
 import os
 import subprocess
@@ -29,7 +30,7 @@ def run_check(case, n):
 def test_two_gpus_match_one(case):
     r = run_check(case, 2)
     for rk in r["ranks"]:
-        for mode in ("mode0", "mode1"):
+        for mode in ("mode0", "mode1", "mode2"):
             m = rk[mode]
             assert m["n_local"] > 0
             assert m["matvec_rel"] < 1e-6, m
@@ -39,4 +40,4 @@ def test_two_gpus_match_one(case):
             assert abs(g / o - 1) < 1e-6 and abs(gi - oi) <= 1, m
             assert abs(m["bibee"][0] / m["bibee"][1] - 1) < 1e-6, m
             assert m["phi_rel"] < 1e-6, m
-        assert rk["self_term"] < 1e-6 and rk["near_mode_leaf_points"] < 1e-6, rk
+        assert rk["self_term"] < 1e-6 and rk["near_mode_leaf_points"] < 1e-6 and rk["quad_points"] < 1e-6, rk

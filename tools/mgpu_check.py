@@ -59,9 +59,14 @@ def main():
     r1 = s1.solve()
     b1 = s1.bibee("cfa")
     phi1 = s1.reaction_potential(r1["sigma"])
-    for mode in (0, 1):
-        c = cfg if mode == 0 else part_of(cfg, rank, world)
-        s = Solver.distributed(c, input_mode=mode, **opts)
+    for mode in (0, 1, 2):  # 2: input_mode 1 with every triangle on rank 0 (the others pass none)
+        if mode == 0:
+            c = cfg
+        elif mode == 1:
+            c = part_of(cfg, rank, world)
+        else:
+            c = cfg if rank == 0 else dict(cfg, vertices=np.zeros((0, 3)), triangles=np.zeros((0, 3), np.int32))
+        s = Solver.distributed(c, input_mode=min(mode, 1), **opts)
         y = gather(s, s.matvec(dev(s, x), "kprime"))
         yd = gather(s, s.matvec(dev(s, x), "double"))  # dipole sources: the halo carries normals
         yh = s.matvec_host(x[s.local_ids].astype(np.float32), "kprime")
@@ -75,7 +80,7 @@ def main():
                                   bibee=(b["dG"], b1["dG"]), phi_rel=rel(phi, phi1))
         s.close()
     # options that need the full mesh (input_mode 0): curvature self-term, analytic near field
-    for kw in (dict(self_term=1), dict(near_mode=1, leaf_points=64)):
+    for kw in (dict(self_term=1), dict(near_mode=1, leaf_points=64), dict(quad_points=3)):
         o = dict(opts, **kw)
         sr = Solver.from_config(cfg, **o)
         yr = sr.to_global(sr.matvec(dev(sr, x), "A").cpu().numpy())
