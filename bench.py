@@ -449,11 +449,14 @@ def main():
                    "d2h_bytes_per_step": 4 * n},
            "comm_ms": ph["comm"],
            "clocks": clocks}
+    free, total = torch.cuda.mem_get_info()
+    out["device_mem_used_gb"] = (total - free) / 1e9  # this process's device (rank 0 with several)
+    out["expansion_slots"] = int(info["expansion_slots"])
+    out["n_cells"] = int(info["n_cells"])
     if dist:  # per-rank breakdown (load balance of the domain decomposition)
-        free, total = torch.cuda.mem_get_info()
         mine = {"rank": rank, "n_local": s.n, "phases_ms": ph, "p2p_interactions": int(tm["p2p_interactions"]),
                 "m2l_pairs": int(tm["m2l_pairs"]), "device_mem_used_gb": (total - free) / 1e9, "setup_s": setup_s,
-                "tree_build_ms": tm["tree"]}
+                "tree_build_ms": tm["tree"], "expansion_slots": int(info["expansion_slots"])}
         allr = [None] * world
         dist.all_gather_object(allr, mine)
         out["per_rank"] = allr

@@ -221,6 +221,8 @@ typedef struct {
   int64_t m2l_pairs;    /* interaction-list entries over all levels */
   double root_width;    /* root cube width (Angstrom) */
   double root_origin[3];
+  int64_t expansion_slots; /* cells with multipole / local storage on this rank: n_cells on one GPU; the
+                              rank's windows + received LET cells with nranks > 1 (FMMBEM_PLAN_CELL_WINDOWS) */
 } fmmbem_tree_info;
 
 fmmbem_status fmmbem_tree_info_get(const fmmbem_ctx* ctx, fmmbem_tree_info* out);
@@ -245,7 +247,14 @@ enum {
   FMMBEM_PLAN_CELL_KEYS = 6,   /* every cell's key, level-major */
   FMMBEM_PLAN_LEVEL_OFFSETS = 7, /* level + 2 offsets into the cell numbering */
   FMMBEM_PLAN_NEIGHBOURS = 8,   /* `peer` = a leaf index: its neighbour leaves (incl. itself) */
-  FMMBEM_PLAN_INTERACTION = 9   /* `peer` = a cell index (level >= 2): its interaction list */
+  FMMBEM_PLAN_INTERACTION = 9,  /* `peer` = a cell index (level >= 2): its interaction list */
+  FMMBEM_PLAN_LET_SEND_CHG = 10,   /* peer: my pure cells whose CHARGE multipoles peer's panels need */
+  FMMBEM_PLAN_LET_RECV_CHG = 11,   /* peer: peer's pure cells whose charge multipoles I need */
+  FMMBEM_PLAN_LET_SHARED_CHG = 12, /* cells with charges straddling ranks (peer ignored) */
+  FMMBEM_PLAN_CELL_WINDOWS = 13,   /* 2 (level + 1) entries: per level l the cells [lo, hi) holding a
+                                      leaf of this rank -- its expansion slots, in that order */
+  FMMBEM_PLAN_EXTRA_CELLS = 14     /* received / shared LET cells outside the windows: the slots
+                                      after the windows' (increasing) */
 };
 fmmbem_status fmmbem_plan_create(const uint64_t* leaf_keys, const int32_t* leaf_panels, const int32_t* leaf_charges,
                                  int64_t n_leaves, int32_t level, int32_t quad_points, int32_t nranks, int32_t rank,

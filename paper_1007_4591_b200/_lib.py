@@ -55,7 +55,8 @@ class Timing(C.Structure):
 class TreeInfo(C.Structure):
     _fields_ = [("levels", C.c_int32), ("n_leaves", C.c_int64), ("n_cells", C.c_int64),
                 ("n_panels", C.c_int64), ("n_charges", C.c_int64), ("nbr_pairs", C.c_int64),
-                ("m2l_pairs", C.c_int64), ("root_width", C.c_double), ("root_origin", C.c_double * 3)]
+                ("m2l_pairs", C.c_int64), ("root_width", C.c_double), ("root_origin", C.c_double * 3),
+                ("expansion_slots", C.c_int64)]
 
 
 # symbol -> (restype, argtypes); every entry point declared in include/fmmbem.h

@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -186,6 +187,36 @@ TgtArg own_targets(fmmbem_ctx* c, bool quad) {
   return t;
 }
 
+// FMMBEM_VERBOSE: device bytes held by the ctx after create, by group, on stderr
+void report_memory(const fmmbem_ctx* c) {
+  auto b = [](const auto& d) { return (double)d.n * sizeof(*d.p); };
+  auto pts = [&](const PointSet& p) { return b(p.pos) + b(p.nrm) + b(p.leaf) + b(p.begin) + b(p.cell_cnt); };
+  const Tree& T = c->tree;
+  double m2lw = 0, items = 0, let = 0;
+  for (const auto& w : c->m2l_cache) m2lw += b(w->idx) + b(w->cell) + b(w->off);
+  for (const auto& w : c->p2p_cache) items += b(w->items);
+  for (const LetPlan* X : {&c->let, &c->let_chg}) {
+    for (const auto& d : X->send) let += b(d);
+    for (const auto& d : X->recv) let += b(d);
+    let += b(X->shared) + b(X->sbuf) + b(X->rbuf) + b(X->shbuf);
+  }
+  const double skel = b(T.key) + b(T.parent) + b(T.child_begin) + b(T.child_end) + b(T.leaf_ijk) + b(c->gbeg) +
+                      b(c->pan_own_cnt) + b(c->quad_own_cnt) + b(c->chg_own_cnt) + b(c->cmap) + b(c->skey);
+  const double lists = b(T.nbr_off) + b(T.nbr_idx) + b(T.m2l_off) + b(T.m2l_idx);
+  const double other = b(c->xext) + b(c->p2p_src) + b(c->halo.sidx) + b(c->halo.sbuf) + b(c->selfd) +
+                       b(c->near.off) + b(c->near.col) + b(c->near.vkp) + b(c->near.vsl) + b(c->near.diag) +
+                       b(c->Itab) + b(c->tmp_x) + b(c->tmp_y) + b(c->chg_ids);
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  std::fprintf(stderr,
+               "[fmmbem rank %d] device GB: points %.3f (panels %.3f, quad %.3f, charges %.3f), expansions %.3f "
+               "(%lld of %lld cells), skeleton %.3f, lists %.3f, M2L work %.3f, P2P items %.3f, LET %.3f, "
+               "other %.3f; device used %.3f\n",
+               c->rank, (pts(c->pan) + pts(c->quad) + pts(c->chg)) / 1e9, pts(c->pan) / 1e9, pts(c->quad) / 1e9,
+               pts(c->chg) / 1e9, (b(c->Mx) + b(c->Lx)) / 1e9, (long long)c->n_slots, (long long)T.n_cells,
+               skel / 1e9, lists / 1e9, m2lw / 1e9, items / 1e9, let / 1e9, other / 1e9, (double)(tot - fr) / 1e9);
+}
+
 }  // namespace
 
 enum : int {
@@ -276,12 +307,9 @@ void fmm_eval(fmmbem_ctx* c, const TgtArg& t, const SrcArg& s, const Outputs& o,
     rec(E_UP1, fs);
     if (distributed) {  // the multipoles this rank's interaction lists need (LET)
       rec(E_AR0, fs);
-      if (c->let.ready) {
-        exchange_let(c, fs);
-      } else {  // fallback: sum every rank's partial multipoles of levels >= 2
-        const size_t off = (size_t)c->tree.lvl_off[2] * c->NC;
-        comm_allreduce_f32(c, reinterpret_cast<float*>(c->Mx.get() + off), 2 * (c->Mx.n - off), fs);
-      }
+      const LetPlan& X = (s.set == &c->chg) ? c->let_chg : c->let;
+      if (!X.ready) throw Error(FMMBEM_E_CUDA, "distributed evaluation without a LET plan");
+      exchange_let(c, X, fs);
       rec(E_AR1, fs);
     }
     const int* tcnt = t.cnt ? t.cnt : t.set->cell_cnt.get();
@@ -375,8 +403,13 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
   }
   FMM_CUDA(cudaMemsetAsync(c->flag.get(), 0, sizeof(int), st));
   TgtArg t = own_targets(c, false);
-  SrcArg s;  // charges are replicated on every rank: full upward sweep, no exchange
+  SrcArg s;  // the charges of this rank's leaves; the other ranks' charge multipoles by the LET
   s.set = &c->chg;
+  if (multi(c)) {
+    s.leaf_lo = c->leaf_lo;
+    s.leaf_hi = c->leaf_hi;
+    s.cnt = c->chg_own_cnt.get();
+  }
   Outputs o;
   o.dn.y = c->En.get() - c->pan_lo;
   o.dn.b = (float)(1.0 / (FOUR_PI * c->eps_in));  // E_n carries 1/eps_I (Eq. 1, reading A2)
@@ -390,10 +423,9 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
   cudaEventRecord(c->ev[E_AG0], st);
   // the charge-on-panel-point check (A14) depends on the geometry only: done at the first evaluation
   const bool check = !c->fields_checked;
-  fmm_eval(c, t, s, o, false, check, st, true, false);
+  fmm_eval(c, t, s, o, false, check, st, true, multi(c));
   cudaEventRecord(c->ev[E_NEAR1], st);
   c->timed_near = true;
-  c->timed_comm = false;
   c->timed_xg = false;
   c->timed_fields = true;
   if (c->K > 1) {
@@ -403,7 +435,7 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
     Outputs oq;
     oq.pot.y = psiq.get();
     oq.pot.b = (float)(1.0 / FOUR_PI);
-    fmm_eval(c, tq, s, oq, false, check, st, false, false);
+    fmm_eval(c, tq, s, oq, false, check, st, false, multi(c));
     if (n > 0)
       k_quad_reduce<<<ceil_div(n, 256), 256, 0, st>>>(n, c->K, psiq.get() + c->pan_lo * c->K,
                                                       c->quad.pos.get() + c->pan_lo * c->K,
@@ -703,17 +735,14 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   build_tree(c, pin, wq.get(), cx.get(), cq.get(), s);  // synchronises s
   c->last.tree = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_tree).count();
   init_tables(c);
-  c->Mx.alloc((size_t)c->tree.n_cells * c->NC);
-  c->Lx.alloc((size_t)c->tree.n_cells * c->NC);
+  c->Mx.alloc((size_t)std::max<int64_t>(c->n_slots, 1) * c->NC);  // rank-local slots (ctx.h)
+  c->Lx.alloc((size_t)std::max<int64_t>(c->n_slots, 1) * c->NC);
   c->red.alloc(64);
   c->flag.alloc(4);
   const PointSet& src = (c->K == 1) ? c->pan : c->quad;
   const bool direct = c->opt.direct != 0 || c->tree.L < 2;
   if (R == 1) c->p2p_inter_kp = count_p2p(c, c->pan, src, true, direct);
-  if (R > 1) {
-    const char* e = std::getenv("FMMBEM_LET");
-    if (!direct && !(e && std::atoi(e) == 0)) build_let(c, c->leaf_bounds, s);
-  }
+  if (R > 1 && !direct) build_let(c, s);
   if (c->opt.near_mode == 1) {
     if (R > 1) {  // the analytic near field needs FP64 geometry of every local (owned + halo) panel
       cen.alloc(3 * nt);
@@ -745,6 +774,7 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   c->p2p_wmax.alloc(1);
   c->p2p_counter.alloc(1);
   FMM_CUDA(cudaStreamSynchronize(s));
+  if (std::getenv("FMMBEM_VERBOSE")) report_memory(c);
   *out = c;
   return FMMBEM_OK;
   }
@@ -1107,6 +1137,7 @@ fmmbem_status fmmbem_tree_info_get(const fmmbem_ctx* c, fmmbem_tree_info* o) {
   o->m2l_pairs = c->tree.m2l_pairs;
   o->root_width = c->tree.W;
   for (int d = 0; d < 3; ++d) o->root_origin[d] = c->tree.x0[d];
+  o->expansion_slots = c->n_slots;
   return FMMBEM_OK;
 }
 

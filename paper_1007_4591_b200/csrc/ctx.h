@@ -35,7 +35,8 @@ struct Tree {
   DevBuf<int> nbr_off, nbr_idx;  // leaf-level neighbour CSR (leaf indices, incl. self)
   DevBuf<long long> m2l_off;     // [n_cells+1] interaction-list CSR offsets (64-bit: > 2^31 entries at 1e9 panels)
   DevBuf<int> m2l_idx;           // global source cell index of each interaction-list entry
-  int64_t nbr_pairs = 0, m2l_pairs = 0;
+  int64_t nbr_pairs = 0, m2l_pairs = 0;  // list entries of the whole tree (the device lists of a rank
+                                          // of several hold its owned leaves' / windows' entries only)
   double width(int l) const { return W / (double)(1LL << l); }
 };
 
@@ -113,7 +114,17 @@ struct fmmbem_ctx {
   std::vector<int64_t> pan_ids;     // local -> caller triangle index
   fmm::DevBuf<int> chg_ids;         // local charge -> caller charge index
 
-  fmm::DevBuf<float2> Mx, Lx;       // expansions [n_cells * NC]
+  // expansions [n_slots * NC]: slot_base[l] + (cell - win_lo[l]) for the cells of level l in this
+  // rank's window, then the LET cells received / shared from outside it (plan.h slot_layout); one
+  // GPU: slot = cell.  lvl_ptr(X, l) addresses a level's window by GLOBAL cell index.
+  fmm::DevBuf<float2> Mx, Lx;
+  std::vector<int64_t> win_lo, win_hi, slot_base;  // [L + 1]
+  int64_t n_slots = 0;
+  fmm::DevBuf<int> cmap;            // [n_cells] cell -> slot or -1 (nranks > 1; empty on one GPU)
+  fmm::DevBuf<uint64_t> skey;       // [n_slots] Morton key of each slot (nranks > 1)
+  const int* slot_map() const { return cmap.n ? cmap.get() : nullptr; }
+  const uint64_t* slot_keys() const { return skey.n ? skey.get() : tree.key.get(); }
+  float2* lvl_ptr(float2* X, int l) const { return X + (slot_base[l] - win_lo[l]) * NC; }
   fmm::DevBuf<float2> Itab;         // M2L irregular-harmonic table [343 * NI]
   int NI = 0;
   fmm::DevBuf<float> tmp_x, tmp_y;  // host-buffer matvec staging / scratch
@@ -156,7 +167,8 @@ struct fmmbem_ctx {
   fmm::DevBuf<int> pan_own_cnt, quad_own_cnt, chg_own_cnt;  // subtree counts of owned points
   fmm::DevBuf<float> selfd;                    // [np] curvature self-term K'_ii in local order (self_term = 1)
   fmm::NearCSR near;                           // near_mode = 1 corrections
-  fmm::LetPlan let;                            // multipole LET exchange plan (nranks > 1)
+  fmm::LetPlan let;                            // multipole LET exchange plan (nranks > 1), panel sources
+  fmm::LetPlan let_chg;                        // ... charge sources (the charge-FMM)
   std::vector<int64_t> leaf_bounds;            // [nranks + 1] leaf partition
   fmm::DevBuf<int> gbeg;                       // [n_leaves + 1] GLOBAL panel CSR over leaves (all ranks)
   fmm::HaloPlan halo;                          // near-field halo exchange (nranks > 1)

@@ -148,8 +148,10 @@ void launch_p2m_dipole(fmmbem_ctx* c, const SrcArg& s, int lo, int hi, cudaStrea
   const Tree& T = c->tree;
   if (T.L < 2 || hi <= lo) return;
   if (c->P > 16 || c->P * (c->P + 1) / 2 > 256) throw Error(FMMBEM_E_INVALID, "dipole P2M: terms too large");
+  check_leaf_window(c, lo, hi);
   k_p2m_dipole<<<hi - lo, 128, 0, st>>>(s.set->pos.get(), c->pan.nrm.get(), s.x, s.set->div, s.set->begin.get(),
-                                        c->P, (float)(1.0 / T.width(T.L)), (int)T.lvl_off[T.L], lo, c->Mx.get());
+                                        c->P, (float)(1.0 / T.width(T.L)), (int)T.lvl_off[T.L], lo,
+                                        c->lvl_ptr(c->Mx.get(), T.L));
   FMM_CHECK_LAUNCH();
 }
 

@@ -118,9 +118,11 @@ __global__ void __launch_bounds__(128) k_p2m(const float4* __restrict__ pos, con
 }
 
 // ---------------------------------------------------------------- M2M
+// Mc / Mp: the child / parent level's expansions addressed by global cell index (ctx.h lvl_ptr)
 __global__ void __launch_bounds__(64) k_m2m(int lvl_off, int P, const int* __restrict__ cb,
                                             const int* __restrict__ ce, const uint64_t* __restrict__ key,
-                                            const int* __restrict__ scnt, float2* __restrict__ M) {
+                                            const int* __restrict__ scnt, const float2* __restrict__ Mc,
+                                            float2* __restrict__ M) {
   extern __shared__ float2 smc[];  // [8][NC] children, then [8][NC] R(d_octant)
   __shared__ int oct[8];
   const int cell = lvl_off + blockIdx.x;
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(64) k_m2m(int lvl_off, int P, const int* __res
   const int c0 = cb[cell], nch = ce[cell] - c0;
   for (int t = threadIdx.x; t < nch * NC; t += blockDim.x) {
     int ch = t / NC, c = t - ch * NC;
-    smc[ch * NC + c] = M[(size_t)(c0 + ch) * NC + c];
+    smc[ch * NC + c] = scnt[c0 + ch] ? Mc[(size_t)(c0 + ch) * NC + c] : make_float2(0.f, 0.f);
   }
   if (threadIdx.x < nch) oct[threadIdx.x] = (int)(key[c0 + threadIdx.x] & 7);
   __syncthreads();
@@ -166,11 +168,12 @@ __global__ void __launch_bounds__(64) k_m2m(int lvl_off, int P, const int* __res
 constexpr int M2L_TPB = 64;
 constexpr int M2L_SB = 4;  // sources staged per step
 
+// cmap: cell -> expansion slot (nullptr: slot = cell), ctx.h
 __global__ void __launch_bounds__(M2L_TPB) k_m2l(int cell_off, int P, const long long* __restrict__ off,
                                                  const int* __restrict__ idx, const uint64_t* __restrict__ key,
                                                  const int* __restrict__ scnt, const int* __restrict__ tcnt,
-                                                 const float2* __restrict__ M, const float2* __restrict__ Itab,
-                                                 float2* __restrict__ Lx) {
+                                                 const int* __restrict__ cmap, const float2* __restrict__ M,
+                                                 const float2* __restrict__ Itab, float2* __restrict__ Lx) {
   extern __shared__ float2 sm[];
   const int NC = P * (P + 1) / 2, NF = P * P, NIF = (2 * P - 1) * (2 * P - 1);
   float2* Mf = sm;                    // [SB][NF]   full M~ (all m)
@@ -195,7 +198,7 @@ __global__ void __launch_bounds__(M2L_TPB) k_m2l(int cell_off, int P, const long
         for (int t = threadIdx.x; t < NIF; t += M2L_TPB) Iq[t] = make_float2(0.f, 0.f);
         continue;
       }
-      const float2* Ms = M + (size_t)s * NC;
+      const float2* Ms = M + (size_t)(cmap ? cmap[s] : s) * NC;
       for (int t = threadIdx.x; t < NF; t += M2L_TPB) {
         int n = 0;
         while ((n + 1) * (n + 1) <= t) ++n;
@@ -239,18 +242,20 @@ __global__ void __launch_bounds__(M2L_TPB) k_m2l(int cell_off, int P, const long
       while ((j + 1) * (j + 2) / 2 <= c) ++j;
       const int k = c - j * (j + 1) / 2;
       const float sg = ((j + k) & 1) ? -1.f : 1.f;
-      float2 v = Lx[(size_t)cell * NC + c];
+      const size_t t = (size_t)(cmap ? cmap[cell] : cell) * NC + c;
+      float2 v = Lx[t];
       v.x = fmaf(sg, acc[o].x, v.x);
       v.y = fmaf(sg, acc[o].y, v.y);
-      Lx[(size_t)cell * NC + c] = v;
+      Lx[t] = v;
     }
   }
 }
 
 // ---------------------------------------------------------------- L2L
+// Lp / Lx: the parent / child level's local expansions addressed by global cell index (ctx.h lvl_ptr)
 __global__ void __launch_bounds__(64) k_l2l(int lvl_off, int P, const int* __restrict__ parent,
                                             const uint64_t* __restrict__ key, const int* __restrict__ tcnt,
-                                            float2* __restrict__ Lx) {
+                                            const float2* __restrict__ Lp, float2* __restrict__ Lx) {
   extern __shared__ float2 sp[];  // parent L~ [NC], then R(d_octant) [NC]
   const int cell = lvl_off + blockIdx.x;
   if (tcnt[cell] == 0) return;
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(64) k_l2l(int lvl_off, int P, const int* __res
   const int oc = (int)(key[cell] & 7);
   float2* R = sp + NC;
   for (int t = threadIdx.x; t < NC; t += blockDim.x) {
-    sp[t] = Lx[(size_t)p * NC + t];
+    sp[t] = Lp[(size_t)p * NC + t];
     R[t] = c_R8[oc][t];
   }
   __syncthreads();
@@ -420,17 +425,27 @@ void init_tables(fmmbem_ctx* c) {
   c->NI = NIF;
 }
 
+// leaf-level kernels address the leaves [lo, hi) through the rank's leaf window (ctx.h)
+void check_leaf_window(const fmmbem_ctx* c, int lo, int hi) {
+  const Tree& T = c->tree;
+  const int64_t a = T.lvl_off[T.L] + lo, b = T.lvl_off[T.L] + hi;
+  if (hi > lo && (a < c->win_lo[T.L] || b > c->win_hi[T.L]))
+    throw Error(FMMBEM_E_INVALID, "leaf range outside this rank's expansion window");
+}
+
 void launch_p2m_range(fmmbem_ctx* c, const SrcArg& s, int lo, int hi, cudaStream_t st) {
   const Tree& T = c->tree;
   const int L = T.L, P = c->P;
   if (L < 2 || hi <= lo) return;
   const PointSet& S = *s.set;
+  check_leaf_window(c, lo, hi);
+  float2* M = c->lvl_ptr(c->Mx.get(), L);
   if (exp_specialised(P)) {
     launch_p2m_t(P, hi - lo, S.pos.get(), s.x, S.div, S.begin.get(), (float)(1.0 / T.width(L)), (int)T.lvl_off[L],
-                 lo, c->Mx.get(), st);
+                 lo, M, st);
   } else {
     k_p2m<<<hi - lo, 128, 0, st>>>(S.pos.get(), s.x, S.div, S.begin.get(), P, (float)(1.0 / T.width(L)),
-                                   (int)T.lvl_off[L], lo, c->Mx.get());
+                                   (int)T.lvl_off[L], lo, M);
     FMM_CHECK_LAUNCH();
   }
 }
@@ -450,14 +465,16 @@ void launch_m2m_levels(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st) {
   const int* cnt = s.cnt ? s.cnt : s.set->cell_cnt.get();
   const bool rot = c->m2l_mode == 0 && m2m_rot_supported(P);
   if (rot) init_rot_tables();
-  for (int l = L - 1; l >= 2; --l) {
+  for (int l = L - 1; l >= 2; --l) {  // the parents of this rank's window
     if (rot) {  // Lx is free during the upward sweep: scratch for the per-child translations
       launch_m2m_rot(c, l, cnt, c->Lx.get(), st);
       continue;
     }
-    int n = (int)(T.lvl_off[l + 1] - T.lvl_off[l]);
-    k_m2m<<<n, 64, 16 * NC * sizeof(float2), st>>>((int)T.lvl_off[l], P, T.child_begin.get(), T.child_end.get(),
-                                                   T.key.get(), cnt, c->Mx.get());
+    const int n = (int)(c->win_hi[l] - c->win_lo[l]);
+    if (n <= 0) continue;
+    k_m2m<<<n, 64, 16 * NC * sizeof(float2), st>>>((int)c->win_lo[l], P, T.child_begin.get(), T.child_end.get(),
+                                                   T.key.get(), cnt, c->lvl_ptr(c->Mx.get(), l + 1),
+                                                   c->lvl_ptr(c->Mx.get(), l));
     FMM_CHECK_LAUNCH();
   }
 }
@@ -480,7 +497,7 @@ void launch_m2l(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStrea
     attr = true;
   }
   k_m2l<<<n, M2L_TPB, smem, st>>>((int)T.lvl_off[2], P, T.m2l_off.get(), T.m2l_idx.get(), T.key.get(), src_cnt,
-                                   tgt_cnt, c->Mx.get(), c->Itab.get(), c->Lx.get());
+                                   tgt_cnt, c->slot_map(), c->Mx.get(), c->Itab.get(), c->Lx.get());
   FMM_CHECK_LAUNCH();
 }
 
@@ -495,9 +512,10 @@ void launch_downward(fmmbem_ctx* c, const int* tgt_cnt, cudaStream_t st) {
       launch_l2l_rot(c, l, tgt_cnt, st);
       continue;
     }
-    int n = (int)(T.lvl_off[l + 2] - T.lvl_off[l + 1]);
-    k_l2l<<<n, 64, 2 * NC * sizeof(float2), st>>>((int)T.lvl_off[l + 1], P, T.parent.get(), T.key.get(), tgt_cnt,
-                                                  c->Lx.get());
+    const int n = (int)(c->win_hi[l + 1] - c->win_lo[l + 1]);  // the children in this rank's window
+    if (n <= 0) continue;
+    k_l2l<<<n, 64, 2 * NC * sizeof(float2), st>>>((int)c->win_lo[l + 1], P, T.parent.get(), T.key.get(), tgt_cnt,
+                                                  c->lvl_ptr(c->Lx.get(), l), c->lvl_ptr(c->Lx.get(), l + 1));
     FMM_CHECK_LAUNCH();
   }
 }
@@ -509,13 +527,15 @@ void launch_l2p(fmmbem_ctx* c, const TgtArg& t, const Outputs& o, cudaStream_t s
   const PointSet& S = *t.set;
   const int lo = t.leaf_lo, hi = t.leaf_hi < 0 ? (int)T.n_leaves : t.leaf_hi;
   if (hi <= lo) return;
+  check_leaf_window(c, lo, hi);
+  const float2* Lw = c->lvl_ptr(c->Lx.get(), L);
   if (exp_specialised(c->P)) {
     launch_l2p_t(c->P, hi - lo, S.pos.get(), S.nrm.get(), S.begin.get(), (float)(1.0 / T.width(L)),
-                 (int)T.lvl_off[L], lo, c->Lx.get(), o.pot, o.dn, st);
+                 (int)T.lvl_off[L], lo, Lw, o.pot, o.dn, st);
     return;
   }
   k_l2p<<<hi - lo, 128, 0, st>>>(S.pos.get(), S.nrm.get(), S.begin.get(), c->P, (float)(1.0 / T.width(L)),
-                                 (int)T.lvl_off[L], lo, c->Lx.get(), o.pot, o.dn);
+                                 (int)T.lvl_off[L], lo, Lw, o.pot, o.dn);
   FMM_CHECK_LAUNCH();
 }
 

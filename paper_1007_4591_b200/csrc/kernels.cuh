@@ -78,8 +78,8 @@ void comm_alltoallv_bytes(fmmbem_ctx* c, const std::vector<const void*>& sbuf, c
                           bool second = false);
 void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std::vector<size_t>& scnt,
                        const std::vector<float*>& rbuf, const std::vector<size_t>& rcnt, cudaStream_t s);
-void build_let(fmmbem_ctx* c, const std::vector<int64_t>& leaf_bounds, cudaStream_t s);
-void exchange_let(fmmbem_ctx* c, cudaStream_t s);
+void build_let(fmmbem_ctx* c, cudaStream_t s);
+void exchange_let(fmmbem_ctx* c, const LetPlan& X, cudaStream_t s);
 // exact interaction count of launch_p2p(t, s) (list mode) -- setup-time helper
 int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self, bool direct, int leaf_lo = 0,
                   int leaf_hi = -1);
@@ -88,6 +88,7 @@ int64_t count_p2p(fmmbem_ctx* c, const PointSet& t, const PointSet& s, bool self
 void launch_upward(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
 // the two halves of launch_upward: P2M over leaves [lo, hi) (Mx must be zeroed first), then M2M
 void launch_p2m_range(fmmbem_ctx* c, const SrcArg& s, int lo, int hi, cudaStream_t st);
+void check_leaf_window(const fmmbem_ctx* c, int lo, int hi);  // throws unless [lo, hi) has expansion slots
 void launch_m2m_levels(fmmbem_ctx* c, const SrcArg& s, cudaStream_t st);
 void launch_m2l(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, cudaStream_t st);
 void launch_downward(fmmbem_ctx* c, const int* tgt_cnt, cudaStream_t st);

@@ -10,7 +10,9 @@
 //     holding p's panels) and that rank r owns is sent r -> p with grouped ncclSend / ncclRecv;
 //   * the few shared cells are summed with one small ncclAllReduce.
 // The lists are derived identically on every rank from the replicated tree and partition, in
-// increasing cell order, so sender and receiver agree without any handshake.
+// increasing cell order, so sender and receiver agree without any handshake.  Multipoles live in
+// the rank's expansion slots (plan.h slot_layout): the lists are stored as slots.  The charge-FMM
+// has its own pair of lists (cells with charges that the panels of a peer need).
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -36,18 +38,25 @@ __global__ void k_unpack(int n, int NC, const int* __restrict__ cells, const flo
 
 }  // namespace
 
-// device copies of the host plan's LET cell lists (plan.cu; identical derivation on every rank)
-void build_let(fmmbem_ctx* c, const std::vector<int64_t>& leaf_bounds, cudaStream_t s) {
-  (void)leaf_bounds;
+namespace {
+
+// device copies of one pair of LET cell lists, as expansion SLOTS (plan.h slot_layout)
+void build_one(fmmbem_ctx* c, LetPlan& X, const std::vector<std::vector<int>>& snd,
+               const std::vector<std::vector<int>>& rcv, const std::vector<int>& shr, cudaStream_t s) {
   const int R = c->nranks, me = c->rank;
-  auto& X = c->let;
   const ExchangePlan& P = c->xplan;
   X.ready = false;
-  if (R <= 1 || c->tree.L < 2) return;
   auto up = [&](const std::vector<int>& v, DevBuf<int>& d) {
-    d.alloc(std::max<size_t>(v.size(), 1));
-    if (!v.empty()) FMM_CUDA(cudaMemcpyAsync(d.get(), v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-    return (int)v.size();
+    std::vector<int> sl(v.size());
+    for (size_t i = 0; i < v.size(); ++i) {
+      const int64_t k = P.slot(v[i]);
+      if (k < 0) throw Error(FMMBEM_E_CUDA, "LET cell without an expansion slot");
+      sl[i] = (int)k;
+    }
+    d.alloc(std::max<size_t>(sl.size(), 1));
+    if (!sl.empty()) FMM_CUDA(cudaMemcpyAsync(d.get(), sl.data(), sl.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    return (int)sl.size();
   };
   X.send.clear();
   X.recv.clear();
@@ -58,24 +67,33 @@ void build_let(fmmbem_ctx* c, const std::vector<int64_t>& leaf_bounds, cudaStrea
   int64_t ts = 0, tr = 0;
   for (int p = 0; p < R; ++p) {
     if (p == me) continue;
-    X.nsend[p] = up(P.let_send[p], X.send[p]);
-    X.nrecv[p] = up(P.let_recv[p], X.recv[p]);
+    X.nsend[p] = up(snd[p], X.send[p]);
+    X.nrecv[p] = up(rcv[p], X.recv[p]);
     ts += X.nsend[p];
     tr += X.nrecv[p];
   }
-  X.nshared = up(P.let_shared, X.shared);
+  X.nshared = up(shr, X.shared);
   X.sbuf.alloc(std::max<int64_t>(ts, 1) * c->NC);
   X.rbuf.alloc(std::max<int64_t>(tr, 1) * c->NC);
   X.shbuf.alloc(std::max<int64_t>(X.nshared, 1) * c->NC);
   X.cells_sent = ts;
   X.cells_recv = tr;
-  FMM_CUDA(cudaStreamSynchronize(s));
   X.ready = true;
 }
 
+}  // namespace
+
+// the LET plans of the panel and the charge multipoles (plan.cu; identical derivation on every rank)
+void build_let(fmmbem_ctx* c, cudaStream_t s) {
+  c->let.ready = c->let_chg.ready = false;
+  if (c->nranks <= 1 || c->tree.L < 2) return;
+  const ExchangePlan& P = c->xplan;
+  build_one(c, c->let, P.let_send, P.let_recv, P.let_shared, s);
+  build_one(c, c->let_chg, P.let_send_chg, P.let_recv_chg, P.let_shared_chg, s);
+}
+
 // the multipole part of the LET: pure cells point to point, shared cells summed
-void exchange_let(fmmbem_ctx* c, cudaStream_t s) {
-  auto& X = c->let;
+void exchange_let(fmmbem_ctx* c, const LetPlan& X, cudaStream_t s) {
   const int R = c->nranks, NC = c->NC;
   float2* M = c->Mx.get();
   int64_t so = 0;

@@ -592,7 +592,7 @@ __global__ void k_m2m_sum(int c0, int n, int NC, const int* __restrict__ cb, con
 template <int P>
 __global__ void __launch_bounds__(32) k_l2l_rot(int c0, int n, const uint64_t* __restrict__ key,
                                                 const int* __restrict__ parent, const int* __restrict__ tcnt,
-                                                float2* __restrict__ Lx) {
+                                                const float2* __restrict__ Lp, float2* __restrict__ Lx) {
   constexpr int NC = P * (P + 1) / 2;
   __shared__ float2 sv[NC * 33];
   __shared__ int on[32];
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(32) k_l2l_rot(int c0, int n, const uint64_t* _
   if (act) {
     float zar[P], zai[P], zbr[P], zbi[P];
     octant_phases<P>(key[cell], zar, zai, zbr, zbi);
-    rot_pass<P, 0, 2, 3, 0>(sl, Lx + (size_t)parent[cell] * NC, zar, zai, zbr, zbi);
+    rot_pass<P, 0, 2, 3, 0>(sl, Lp + (size_t)parent[cell] * NC, zar, zai, zbr, zbi);
     coax_l2l<P, 0>(sl);
     rot_pass<P, 0, 2, 3, 4>(sl, nullptr, zar, zai, zbr, zbi);
   }
@@ -643,9 +643,11 @@ __global__ void k_compact_count(int n, int cell_off, const long long* __restrict
   cnt[i] = m;
 }
 
+// the compacted lists hold expansion SLOTS (cmap: cell -> slot, nullptr = identity; ctx.h); a
+// needed cell without a slot (a LET plan that missed it) raises flag
 __global__ void k_compact_fill(int n, int cell_off, const long long* __restrict__ off, const int* __restrict__ idx,
-                               const int* __restrict__ scnt, const int* __restrict__ pos, int* out_idx,
-                               int* out_cell, int* out_off) {
+                               const int* __restrict__ scnt, const int* __restrict__ pos, const int* __restrict__ cmap,
+                               int* out_idx, int* out_cell, int* out_off, int* flag) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int c = cell_off + i;
@@ -653,9 +655,15 @@ __global__ void k_compact_fill(int n, int cell_off, const long long* __restrict_
   if (start == end) return;
   int w = start;
   for (long long e = off[c]; e < off[c + 1]; ++e)
-    if (scnt[idx[e]] > 0) out_idx[w++] = idx[e];
+    if (scnt[idx[e]] > 0) {
+      const int sl = cmap ? cmap[idx[e]] : idx[e];
+      if (sl < 0) atomicOr(flag, 1);
+      out_idx[w++] = sl < 0 ? 0 : sl;
+    }
   // row r of the compacted list = number of non-empty rows before i
-  out_cell[pos[n + 1 + i]] = c;
+  const int tc = cmap ? cmap[c] : c;
+  if (tc < 0) atomicOr(flag, 1);
+  out_cell[pos[n + 1 + i]] = tc < 0 ? 0 : tc;
   out_off[pos[n + 1 + i]] = start;
 }
 
@@ -731,11 +739,18 @@ const M2LWork& m2l_work(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, c
   w->idx.alloc(std::max(1, h[0]));
   w->cell.alloc(std::max(1, h[1]));
   w->off.alloc(h[1] + 1);
+  DevBuf<int> flag;
+  flag.alloc(1);
+  flag.zero(st);
   k_compact_fill<<<ceil_div(n, 256), 256, 0, st>>>(n, off0, T.m2l_off.get(), T.m2l_idx.get(), src_cnt, pos.get(),
-                                                    w->idx.get(), w->cell.get(), w->off.get());
+                                                    c->slot_map(), w->idx.get(), w->cell.get(), w->off.get(),
+                                                    flag.get());
   FMM_CHECK_LAUNCH();
   FMM_CUDA(cudaMemcpyAsync(w->off.get() + h[1], &h[0], sizeof(int), cudaMemcpyHostToDevice, st));
+  int bad = 0;
+  FMM_CUDA(cudaMemcpyAsync(&bad, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
+  if (bad) throw Error(FMMBEM_E_CUDA, "M2L source or target cell without an expansion slot (LET plan)");
   c->m2l_cache.push_back(std::move(w));
   return *c->m2l_cache.back();
 }
@@ -743,35 +758,43 @@ const M2LWork& m2l_work(fmmbem_ctx* c, const int* src_cnt, const int* tgt_cnt, c
 bool m2m_rot_supported(int P) { return rot_supported(P); }
 
 // M2M of level l (children at l + 1); scratch T must hold n_cells * NC float2
+// (the cells of this rank's windows only: children of level l + 1, parents of level l; pointers by
+// global cell index through lvl_ptr, ctx.h)
 void launch_m2m_rot(fmmbem_ctx* c, int l, const int* scnt, float2* T, cudaStream_t st) {
   const Tree& Tr = c->tree;
-  const int ch0 = (int)Tr.lvl_off[l + 1], nch = (int)(Tr.lvl_off[l + 2] - Tr.lvl_off[l + 1]);
-  const int p0 = (int)Tr.lvl_off[l], np = (int)(Tr.lvl_off[l + 1] - Tr.lvl_off[l]);
+  const int ch0 = (int)c->win_lo[l + 1], nch = (int)(c->win_hi[l + 1] - c->win_lo[l + 1]);
+  const int p0 = (int)c->win_lo[l], np = (int)(c->win_hi[l] - c->win_lo[l]);
+  if (nch <= 0 || np <= 0) return;
+  const float2* Mc = c->lvl_ptr(c->Mx.get(), l + 1);
+  float2* Tc = c->lvl_ptr(T, l + 1);
   switch (c->P) {
-    case 8: k_m2m_rot<8><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
-    case 10: k_m2m_rot<10><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
-    case 12: k_m2m_rot<12><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
-    case 13: k_m2m_rot<13><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
-    case 14: k_m2m_rot<14><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, c->Mx.get(), T); break;
+    case 8: k_m2m_rot<8><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, Mc, Tc); break;
+    case 10: k_m2m_rot<10><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, Mc, Tc); break;
+    case 12: k_m2m_rot<12><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, Mc, Tc); break;
+    case 13: k_m2m_rot<13><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, Mc, Tc); break;
+    case 14: k_m2m_rot<14><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), scnt, Mc, Tc); break;
     default: throw Error(FMMBEM_E_INVALID, "M2M rotation not instantiated for this P");
   }
   k_m2m_sum<<<ceil_div((int64_t)np * c->NC, 256), 256, 0, st>>>(p0, np, c->NC, Tr.child_begin.get(),
-                                                                 Tr.child_end.get(), scnt, T, c->Mx.get());
+                                                                 Tr.child_end.get(), scnt, Tc,
+                                                                 c->lvl_ptr(c->Mx.get(), l));
   FMM_CHECK_LAUNCH();
 }
 
 // L2L from level l to l + 1
 void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st) {
   const Tree& Tr = c->tree;
-  const int ch0 = (int)Tr.lvl_off[l + 1], nch = (int)(Tr.lvl_off[l + 2] - Tr.lvl_off[l + 1]);
+  const int ch0 = (int)c->win_lo[l + 1], nch = (int)(c->win_hi[l + 1] - c->win_lo[l + 1]);
+  if (nch <= 0) return;
+  const float2* Lp = c->lvl_ptr(c->Lx.get(), l);
+  float2* Lc = c->lvl_ptr(c->Lx.get(), l + 1);
+#define FMM_L2L_CASE(PP) \
+  case PP: k_l2l_rot<PP><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, Lp, Lc); break;
   switch (c->P) {
-    case 8: k_l2l_rot<8><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
-    case 10: k_l2l_rot<10><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
-    case 12: k_l2l_rot<12><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
-    case 13: k_l2l_rot<13><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
-    case 14: k_l2l_rot<14><<<ceil_div(nch, 32), 32, 0, st>>>(ch0, nch, Tr.key.get(), Tr.parent.get(), tcnt, c->Lx.get()); break;
+    FMM_L2L_CASE(8) FMM_L2L_CASE(10) FMM_L2L_CASE(12) FMM_L2L_CASE(13) FMM_L2L_CASE(14)
     default: throw Error(FMMBEM_E_INVALID, "L2L rotation not instantiated for this P");
   }
+#undef FMM_L2L_CASE
   FMM_CHECK_LAUNCH();
 }
 
@@ -788,7 +811,7 @@ void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem
     attr_devices |= 1ULL << dev;
   }
   k_m2l_rot_sync<P, W, M2L_RPW><<<ceil_div(w.rows, M2L_RPW * W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
-                                                                   w.idx.get(), T.key.get(), c->Mx.get(),
+                                                                   w.idx.get(), c->slot_keys(), c->Mx.get(),
                                                                    c->Lx.get());
 }
 
@@ -811,7 +834,7 @@ void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
       m2l_sync_launch<PP, W>(w, T, c, (size_t)W * (PP * (PP + 1) / 2) * 33 * sizeof(float2), st);        \
     } else {                                                                                               \
       k_m2l_rot<PP, 1><<<(int)w.rows, 32, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(), w.idx.get(),   \
-                                                   T.key.get(), c->Mx.get(), c->Lx.get());                 \
+                                                   c->slot_keys(), c->Mx.get(), c->Lx.get());              \
     }                                                                                                      \
     break;
   switch (c->P) {

@@ -141,7 +141,9 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
   }
   (void)lo;
   (void)hi;
-  // local essential tree: leaf range and owner of every cell (levels >= 2), sources per cell
+  // local essential tree: leaf range and owner of every cell (levels >= 2), sources per cell.
+  // Panel multipoles serve every target point (K', V, A at panels; the reaction potential at the
+  // charges); charge multipoles serve the panels (E_n, psi of the charge-FMM).
   std::vector<long long> tpre(nl + 1, 0), ppre(nl + 1, 0);
   for (int64_t k = 0; k < nl; ++k) {
     tpre[k + 1] = tpre[k] + leaf_tgt[k];
@@ -149,7 +151,7 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
   }
   const int64_t c0 = T.lvl_off[std::min(2, L + 1)];
   std::vector<int> first(nc, 0), end(nc, 0), owner(nc, -1);
-  std::vector<char> has_src(nc, 0);
+  std::vector<char> has_src(nc, 0), has_chg(nc, 0);
   for (int64_t c = c0; c < nc; ++c) {
     int l = 0;
     while (c >= T.lvl_off[l + 1]) ++l;
@@ -159,28 +161,39 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
     end[c] = lower_bound_key(T.key, leaf0, T.lvl_off[L + 1], b) - (int)leaf0;
     if (end[c] > first[c] && lrank[first[c]] == lrank[end[c] - 1]) owner[c] = lrank[first[c]];
     has_src[c] = ppre[end[c]] > ppre[first[c]];
+    has_chg[c] = (tpre[end[c]] - tpre[first[c]]) > (ppre[end[c]] - ppre[first[c]]);
   }
   X.let_send.assign(R, {});
   X.let_recv.assign(R, {});
   X.let_shared.clear();
+  X.let_send_chg.assign(R, {});
+  X.let_recv_chg.assign(R, {});
+  X.let_shared_chg.clear();
   // one pass over the interaction lists: need[s] = ranks holding targets below some cell whose list
-  // contains s (a rank-bit mask; set-if-missing atomics, so the lists are split over host threads)
-  std::vector<std::atomic<unsigned long long>> need(nc);
+  // contains s (rank-bit masks; set-if-missing atomics, so the lists are split over host threads)
+  std::vector<std::atomic<unsigned long long>> need(nc), need_c(nc);
   for (auto& v : need) v.store(0, std::memory_order_relaxed);
+  for (auto& v : need_c) v.store(0, std::memory_order_relaxed);
   auto work = [&](int64_t lo_c, int64_t hi_c) {
     for (int64_t c = lo_c; c < hi_c; ++c) {
       if (end[c] <= first[c]) continue;
-      unsigned long long tm = 0;
+      unsigned long long tm = 0, pm = 0;  // ranks with target points / panels below c
       for (int p = lrank[first[c]]; p <= lrank[end[c] - 1]; ++p) {
         const int f = std::max(first[c], (int)X.leaf_bounds[p]), e = std::min(end[c], (int)X.leaf_bounds[p + 1]);
         if (e > f && tpre[e] > tpre[f]) tm |= 1ULL << p;
+        if (e > f && ppre[e] > ppre[f]) pm |= 1ULL << p;
       }
       if (!tm) continue;
       for (int64_t k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k) {
         const int sidx = T.m2l_idx[k];
-        if (!has_src[sidx]) continue;
-        auto& v = need[sidx];
-        if ((v.load(std::memory_order_relaxed) & tm) != tm) v.fetch_or(tm, std::memory_order_relaxed);
+        if (has_src[sidx]) {
+          auto& v = need[sidx];
+          if ((v.load(std::memory_order_relaxed) & tm) != tm) v.fetch_or(tm, std::memory_order_relaxed);
+        }
+        if (pm && has_chg[sidx]) {
+          auto& v = need_c[sidx];
+          if ((v.load(std::memory_order_relaxed) & pm) != pm) v.fetch_or(pm, std::memory_order_relaxed);
+        }
       }
     }
   };
@@ -194,19 +207,71 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
     for (int t = 0; t < nth; ++t) th.emplace_back(work, c0 + ncell * t / nth, c0 + ncell * (t + 1) / nth);
     for (auto& t : th) t.join();
   }
-  for (int64_t c = c0; c < nc; ++c) {
-    const unsigned long long m = need[c].load(std::memory_order_relaxed);
-    if (owner[c] < 0) {
-      if (has_src[c]) X.let_shared.push_back((int)c);
-      continue;
+  auto lists = [&](const std::vector<char>& has, const std::vector<std::atomic<unsigned long long>>& nd,
+                   std::vector<std::vector<int>>& snd, std::vector<std::vector<int>>& rcv, std::vector<int>& shr) {
+    for (int64_t c = c0; c < nc; ++c) {
+      const unsigned long long m = nd[c].load(std::memory_order_relaxed);
+      if (owner[c] < 0) {
+        if (has[c]) shr.push_back((int)c);
+        continue;
+      }
+      if (owner[c] == me) {
+        for (int p = 0; p < R; ++p)
+          if (p != me && (m >> p & 1ULL)) snd[p].push_back((int)c);
+      } else if (m >> me & 1ULL) {
+        rcv[owner[c]].push_back((int)c);
+      }
     }
-    if (owner[c] == me) {
-      for (int p = 0; p < R; ++p)
-        if (p != me && (m >> p & 1ULL)) X.let_send[p].push_back((int)c);
-    } else if (m >> me & 1ULL) {
-      X.let_recv[owner[c]].push_back((int)c);
+  };
+  lists(has_src, need, X.let_send, X.let_recv, X.let_shared);
+  lists(has_chg, need_c, X.let_send_chg, X.let_recv_chg, X.let_shared_chg);
+  slot_layout(T, me, X);
+}
+
+// Windows of this rank's cells per level and the slot numbering (plan.h).  A cell of level l holds
+// a leaf of [lo, hi) iff its key lies between the level-l ancestors of leaves lo and hi - 1.
+void slot_layout(const HostTree& T, int me, ExchangePlan& X) {
+  const int L = T.L;
+  const int64_t leaf0 = T.lvl_off[L];
+  const int64_t lo = X.leaf_bounds[me], hi = X.leaf_bounds[me + 1];
+  X.lvl_off = T.lvl_off;
+  X.win_lo.assign(L + 1, 0);
+  X.win_hi.assign(L + 1, 0);
+  X.slot_base.assign(L + 1, 0);
+  int64_t n = 0;
+  for (int l = 0; l <= L; ++l) {
+    X.win_lo[l] = X.win_hi[l] = T.lvl_off[l];
+    if (hi > lo) {
+      const int sh = 3 * (L - l);
+      X.win_lo[l] = lower_bound_key(T.key, T.lvl_off[l], T.lvl_off[l + 1], T.key[leaf0 + lo] >> sh);
+      X.win_hi[l] = lower_bound_key(T.key, T.lvl_off[l], T.lvl_off[l + 1], T.key[leaf0 + hi - 1] >> sh) + 1;
     }
+    X.slot_base[l] = n;
+    n += X.win_hi[l] - X.win_lo[l];
   }
+  std::vector<int> ex;
+  auto add = [&](const std::vector<int>& v) { ex.insert(ex.end(), v.begin(), v.end()); };
+  for (size_t p = 0; p < X.let_recv.size(); ++p) add(X.let_recv[p]);
+  for (size_t p = 0; p < X.let_recv_chg.size(); ++p) add(X.let_recv_chg[p]);
+  add(X.let_shared);
+  add(X.let_shared_chg);
+  std::sort(ex.begin(), ex.end());
+  ex.erase(std::unique(ex.begin(), ex.end()), ex.end());
+  X.extra.clear();
+  X.n_slots = n;
+  for (int c : ex)
+    if (X.slot(c) < 0) X.extra.push_back(c);
+  X.n_slots = n + (int64_t)X.extra.size();
+}
+
+int64_t ExchangePlan::slot(int64_t c) const {
+  if (c < 0 || lvl_off.empty() || c >= lvl_off.back()) return -1;
+  const int l = (int)(std::upper_bound(lvl_off.begin(), lvl_off.end(), c) - lvl_off.begin()) - 1;
+  if (c >= win_lo[l] && c < win_hi[l]) return slot_base[l] + (c - win_lo[l]);
+  const auto it = std::lower_bound(extra.begin(), extra.end(), (int)c);
+  if (it == extra.end() || *it != c) return -1;
+  const int64_t nw = slot_base.back() + (win_hi.back() - win_lo.back());
+  return nw + (it - extra.begin());
 }
 
 }  // namespace fmm
@@ -255,7 +320,8 @@ int64_t fmmbem_plan_list(const fmmbem_plan* p, int32_t list, int32_t peer, int64
       for (size_t i = 0; i < v.size(); ++i) out[i] = (int64_t)v[i];
     return (int64_t)v.size();
   };
-  const bool per_peer = list >= FMMBEM_PLAN_HALO_SEND && list <= FMMBEM_PLAN_LET_RECV;
+  const bool per_peer = (list >= FMMBEM_PLAN_HALO_SEND && list <= FMMBEM_PLAN_LET_RECV) ||
+                        list == FMMBEM_PLAN_LET_SEND_CHG || list == FMMBEM_PLAN_LET_RECV_CHG;
   if (per_peer && (peer < 0 || peer >= R)) return -1;
   const int64_t nl = T.lvl_off[T.L + 1] - T.lvl_off[T.L], nc = T.lvl_off[T.L + 1];
   if (list == FMMBEM_PLAN_NEIGHBOURS) {
@@ -277,6 +343,18 @@ int64_t fmmbem_plan_list(const fmmbem_plan* p, int32_t list, int32_t peer, int64
     case FMMBEM_PLAN_LEAF_BOUNDS: return emit(X.leaf_bounds);
     case FMMBEM_PLAN_CELL_KEYS: return emit(T.key);
     case FMMBEM_PLAN_LEVEL_OFFSETS: return emit(T.lvl_off);
+    case FMMBEM_PLAN_LET_SEND_CHG: return emit(X.let_send_chg[peer]);
+    case FMMBEM_PLAN_LET_RECV_CHG: return emit(X.let_recv_chg[peer]);
+    case FMMBEM_PLAN_LET_SHARED_CHG: return emit(X.let_shared_chg);
+    case FMMBEM_PLAN_EXTRA_CELLS: return emit(X.extra);
+    case FMMBEM_PLAN_CELL_WINDOWS: {
+      std::vector<int64_t> v;
+      for (size_t l = 0; l < X.win_lo.size(); ++l) {
+        v.push_back(X.win_lo[l]);
+        v.push_back(X.win_hi[l]);
+      }
+      return emit(v);
+    }
     default: return -1;
   }
 }

@@ -23,13 +23,24 @@ struct HostTree {
 struct ExchangePlan {
   std::vector<int64_t> leaf_bounds;                  // [R + 1] contiguous leaf ranges
   std::vector<std::vector<int>> halo_send, halo_recv;  // per peer: leaves (increasing)
-  std::vector<std::vector<int>> let_send, let_recv;    // per peer: pure cells (increasing)
-  std::vector<int> let_shared;                         // cells straddling ranks (with sources)
+  std::vector<std::vector<int>> let_send, let_recv;    // per peer: pure cells (increasing), panel sources
+  std::vector<int> let_shared;                         // cells straddling ranks (with panel sources)
+  std::vector<std::vector<int>> let_send_chg, let_recv_chg;  // the same for charge sources (charge-FMM)
+  std::vector<int> let_shared_chg;
+  // rank-local expansion storage: the cells of level l holding a leaf of this rank form the window
+  // [win_lo[l], win_hi[l]) (contiguous: leaves and cells are in Morton order); they get the slots
+  // slot_base[l] + (cell - win_lo[l]), and the LET cells received or shared that lie outside the
+  // windows (`extra`, increasing) follow them.
+  std::vector<int64_t> lvl_off, win_lo, win_hi, slot_base;  // [L + 2] / [L + 1]
+  std::vector<int> extra;
+  int64_t n_slots = 0;
+  int64_t slot(int64_t cell) const;  // -1: no slot on this rank
 };
 
 void host_tree(const uint64_t* leaf_keys, int64_t nl, int L, HostTree& T);
 void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int K,
                    int R, int me, ExchangePlan& X);
+void slot_layout(const HostTree& T, int me, ExchangePlan& X);  // windows + extra cells (plan_exchange calls it)
 void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds);
 
 }  // namespace fmm

@@ -524,6 +524,68 @@ void build_halo(fmmbem_ctx* c, const std::vector<int>& hgb, DevBuf<float4>& opos
 // positions exchanged here, weights per matvec).  Memory per rank: the slice, the owned panels and
 // the halo (O(N/R)) plus the O(N/leaf_points) skeleton.  With one rank the same steps reduce to the
 // single-GPU build (no exchange).
+// nranks > 1, after the plan: the rank keeps the lists of its own leaves / windows only (the full
+// lists served the plan on the host) and numbers its expansion slots (plan.h slot_layout): cell ->
+// slot map and the slots' keys on the device
+void local_lists_and_slots(fmmbem_ctx* c, const HostTree& H, cudaStream_t s) {
+  Tree& T = c->tree;
+  const ExchangePlan& X = c->xplan;
+  const int L = T.L, nl = (int)T.n_leaves;
+  const int64_t nc = T.n_cells;
+  const int lo = c->leaf_lo, hi = c->leaf_hi;
+  {  // neighbour lists of the owned leaves
+    std::vector<int> off(nl + 1);
+    for (int k = 0; k <= nl; ++k) off[k] = H.nbr_off[std::min(std::max(k, lo), hi)] - H.nbr_off[lo];
+    const int n = off[nl];
+    T.nbr_off.alloc(nl + 1);
+    T.nbr_idx.alloc(std::max(n, 1));
+    FMM_CUDA(cudaMemcpyAsync(T.nbr_off.get(), off.data(), (nl + 1) * sizeof(int), cudaMemcpyHostToDevice, s));
+    if (n) FMM_CUDA(cudaMemcpyAsync(T.nbr_idx.get(), H.nbr_idx.data() + H.nbr_off[lo], n * sizeof(int),
+                                    cudaMemcpyHostToDevice, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+  }
+  {  // interaction lists of the window cells (levels >= 2), one contiguous segment per level
+    std::vector<long long> off(nc + 1, 0);
+    long long n = 0;
+    for (int l = 0; l <= L; ++l)
+      for (int64_t cc = T.lvl_off[l]; cc < T.lvl_off[l + 1]; ++cc) {
+        off[cc] = n;
+        if (cc >= X.win_lo[l] && cc < X.win_hi[l]) n += H.m2l_off[cc + 1] - H.m2l_off[cc];
+      }
+    off[nc] = n;
+    T.m2l_off.release();
+    T.m2l_idx.release();
+    T.m2l_off.alloc(nc + 1);
+    T.m2l_idx.alloc(std::max<long long>(n, 1));
+    FMM_CUDA(cudaMemcpyAsync(T.m2l_off.get(), off.data(), (nc + 1) * sizeof(long long), cudaMemcpyHostToDevice, s));
+    for (int l = 2; l <= L; ++l) {
+      const int64_t a = H.m2l_off[X.win_lo[l]], b = H.m2l_off[X.win_hi[l]];
+      if (b > a)
+        FMM_CUDA(cudaMemcpyAsync(T.m2l_idx.get() + off[X.win_lo[l]], H.m2l_idx.data() + a, (b - a) * sizeof(int),
+                                 cudaMemcpyHostToDevice, s));
+    }
+    FMM_CUDA(cudaStreamSynchronize(s));
+  }
+  // slots
+  c->win_lo = X.win_lo;
+  c->win_hi = X.win_hi;
+  c->slot_base = X.slot_base;
+  c->n_slots = X.n_slots;
+  std::vector<int> cmap(nc, -1);
+  std::vector<uint64_t> skey(std::max<int64_t>(X.n_slots, 1), 0);
+  for (int l = 0; l <= L; ++l)
+    for (int64_t cc = X.win_lo[l]; cc < X.win_hi[l]; ++cc) cmap[cc] = (int)(X.slot_base[l] + cc - X.win_lo[l]);
+  const int64_t nw = X.n_slots - (int64_t)X.extra.size();
+  for (size_t i = 0; i < X.extra.size(); ++i) cmap[X.extra[i]] = (int)(nw + (int64_t)i);
+  for (int64_t cc = 0; cc < nc; ++cc)
+    if (cmap[cc] >= 0) skey[cmap[cc]] = H.key[cc];
+  c->cmap.alloc(nc);
+  c->skey.alloc(skey.size());
+  FMM_CUDA(cudaMemcpyAsync(c->cmap.get(), cmap.data(), nc * sizeof(int), cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaMemcpyAsync(c->skey.get(), skey.data(), skey.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
 void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const double* cxyz, const double* cq,
                 cudaStream_t s) {
   Tree& T = c->tree;
@@ -812,10 +874,19 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
       n_own_p += pan[k];
     }
     c->p2p_inter_kp = own - n_own_p * K;
+    local_lists_and_slots(c, H, s);
   } else {
     c->leaf_bounds = {0, nl};
     c->leaf_lo = 0;
     c->leaf_hi = nl;
+    c->win_lo.assign(L + 1, 0);
+    c->win_hi.assign(L + 1, 0);
+    c->slot_base.assign(L + 1, 0);
+    for (int l = 0; l <= L; ++l) {
+      c->win_lo[l] = c->slot_base[l] = T.lvl_off[l];
+      c->win_hi[l] = T.lvl_off[l + 1];
+    }
+    c->n_slots = T.n_cells;
   }
   const int leaf_lo = c->leaf_lo, leaf_hi = c->leaf_hi;
   std::vector<int> hgb(nl + 1);

@@ -40,4 +40,5 @@ def test_two_gpus_match_one(case):
             assert abs(g / o - 1) < 1e-6 and abs(gi - oi) <= 1, m
             assert abs(m["bibee"][0] / m["bibee"][1] - 1) < 1e-6, m
             assert m["phi_rel"] < 1e-6, m
+            assert 0 < m["slots"] < m["n_cells"], m  # rank-local expansion storage
         assert rk["self_term"] < 1e-6 and rk["near_mode_leaf_points"] < 1e-6 and rk["quad_points"] < 1e-6, rk

@@ -116,8 +116,10 @@ def library_plan(keys, npan, nchg, L, world, rank):
         lib.fmmbem_plan_list(h, kind, peer, out.ctypes.data_as(C.POINTER(C.c_int64)))
         return out[:n].tolist()
 
-    res = {"bounds": lst(5), "cell_keys": lst(6), "lvl_off": lst(7), "shared": lst(4)}
-    for kind, name in ((0, "halo_send"), (1, "halo_recv"), (2, "let_send"), (3, "let_recv")):
+    res = {"bounds": lst(5), "cell_keys": lst(6), "lvl_off": lst(7), "shared": lst(4), "shared_chg": lst(12),
+           "windows": lst(13), "extra": lst(14)}
+    for kind, name in ((0, "halo_send"), (1, "halo_recv"), (2, "let_send"), (3, "let_recv"), (10, "let_send_chg"),
+                       (11, "let_recv_chg")):
         res[name] = [lst(kind, p) for p in range(world)]
     lib.fmmbem_plan_destroy(h)
     return res
@@ -166,36 +168,57 @@ def brute_force_check(plans, keys, npan, nchg, L):
 
     tgt = npan + nchg
     for r in range(R):
-        got = set(plans[r]["shared"])
+        got = set(plans[r]["shared"])      # panel multipoles complete on r besides its pure cells
+        got_c = set(plans[r]["shared_chg"])  # charge multipoles (the charge-FMM's sources)
         for p in range(R):
             if p != r:
                 assert plans[r]["let_recv"][p] == plans[p]["let_send"][r]
+                assert plans[r]["let_recv_chg"][p] == plans[p]["let_send_chg"][r]
                 got |= set(plans[r]["let_recv"][p])
+                got_c |= set(plans[r]["let_recv_chg"][p])
+        # expansion slots: the window of level l = exactly the cells holding a leaf of r (brute force)
+        win = plans[r]["windows"]
+        assert len(win) == 2 * (L + 1)
+        in_win = set()
+        for l in range(L + 1):
+            mine = [off[l] + j for j, k in enumerate(lvl_keys[l]) if (lrank[leaves_below(l, k)] == r).any()]
+            assert list(range(win[2 * l], win[2 * l + 1])) == mine, (r, l)
+            in_win |= set(mine)
+        extra = plans[r]["extra"]
+        assert extra == sorted(extra) and not (set(extra) & in_win)
+        assert set(extra) == (got | got_c) - in_win
+        slots = in_win | set(extra)
         for l in range(2, L + 1):
             cells = lvl_keys[l]
             cx = np.stack(_demorton(cells), 1)
             par = cx >> 1
             for i, t in enumerate(cells):
                 lt = leaves_below(l, t)
-                if not (tgt[lt][lrank[lt] == r] > 0).any():
+                has_t = (tgt[lt][lrank[lt] == r] > 0).any()
+                has_p = (npan[lt][lrank[lt] == r] > 0).any()
+                if not has_t:
                     continue  # no targets of rank r below t
                 near_par = np.abs(par - par[i]).max(1) <= 1
                 far = np.abs(cx - cx[i]).max(1) > 1
                 for j in np.nonzero(near_par & far)[0]:  # interaction list, brute force
                     ls = leaves_below(l, cells[j])
-                    if npan[ls].sum() == 0:
-                        continue
                     gidx = off[l] + j
                     owners = set(lrank[ls].tolist())
+                    if npan[ls].sum() > 0 or (has_p and nchg[ls].sum() > 0):
+                        assert gidx in slots, (r, l, int(t), int(cells[j]))  # its M2L reads a slot
                     if owners == {r}:
                         continue  # pure, computed locally
-                    assert gidx in got, (r, l, int(t), int(cells[j]))
-        # shared = exactly the cells with sources straddling ranks
+                    if npan[ls].sum() > 0:
+                        assert gidx in got, (r, l, int(t), int(cells[j]))
+                    if has_p and nchg[ls].sum() > 0:  # charge sources serve the panels (E_n, psi)
+                        assert gidx in got_c, (r, l, int(t), int(cells[j]))
+    # shared = exactly the cells with sources (panels / charges) straddling ranks
     for l in range(2, L + 1):
         for j, k in enumerate(lvl_keys[l]):
             ls = leaves_below(l, k)
-            straddle = len(set(lrank[ls].tolist())) > 1 and npan[ls].sum() > 0
-            assert ((off[l] + j) in set(plans[0]["shared"])) == straddle
+            straddle = len(set(lrank[ls].tolist())) > 1
+            assert ((off[l] + j) in set(plans[0]["shared"])) == (straddle and npan[ls].sum() > 0)
+            assert ((off[l] + j) in set(plans[0]["shared_chg"])) == (straddle and nchg[ls].sum() > 0)
 
 
 @pytest.mark.parametrize("world", [2, 4])
