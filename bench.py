@@ -431,7 +431,8 @@ def main():
                       "quad_points": 1, "leaf_points": args.leaf_points, "near_mode": args.near_mode,
                       "operator": "V (potential)" if cube else "A = I - f K'",
                       "tree_levels": info["levels"], "n_leaves": info["n_leaves"],
-                      "l2_flush": "inputs larger than L2 (x 409 MB, points 3.3 GB)",
+                      "l2_flush": f"inputs larger than L2 (x {4 * n / 1e6:.0f} MB, points {32 * n / 1e9:.1f} GB "
+                                  "over all ranks; 126 MB L2)",
                       "parallelism": "single GPU" if world == 1 else
                       f"octree domain decomposition x{world} (NCCL: halo x exchange, LET multipole send/recv)"},
            "matvec_s": ms * 1e-3,
