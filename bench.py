@@ -58,14 +58,20 @@ def m2l_rot_flops(P):
     return 4 * mat + 4 * 6 * (NC - P) + coax + 2 * 2 * NC
 
 
-def launches_per_matvec(L, P):
+def launches_per_matvec(L, P, info=None):
     """libfmmbem kernels per A-matvec: P2M, M2M per level (rotation: translate + sum), one M2L,
     L2L per level, the P2P weight normalisation (k_absmax) and scaled source table (k_scale_src),
-    P2P, L2P (memsets and NCCL kernels excluded)."""
+    P2P, L2P (memsets, copies and NCCL kernels excluded).  Several ranks (tree_info of the rank):
+    + the halo weight gather, + one LET pack per peer sent to and one unpack per peer received from,
+    + a pack and an unpack of the shared cells."""
     if L < 2:
         return 3
     m2m = 2 if P in (8, 10, 12, 13, 14) else 1
-    return 1 + m2m * (L - 2) + 1 + (L - 2) + 2 + 1 + 1
+    n = 1 + m2m * (L - 2) + 1 + (L - 2) + 2 + 1 + 1
+    if info is not None and info.get("let_send_peers") is not None:
+        n += int(info["halo_panels_sent"] > 0) + info["let_send_peers"] + info["let_recv_peers"]
+        n += 2 * int(info["let_shared_cells"] > 0)
+    return n
 
 
 ARRAYS = {"c5": (10, 10, 10), "c5_22": (22, 22, 22)}  # C5 and the paper-headline 1.09e9-panel array
@@ -445,7 +451,7 @@ def main():
            "tree_build_ms": tm["tree"],
            "bibee_cfa": bibee,
            "roofline": roof, "roofline_kernels": kern, "hbm_peak_source": hbm_src,
-           "gpu_launches": args.steps * launches_per_matvec(info["levels"], P),
+           "gpu_launches": args.steps * launches_per_matvec(info["levels"], P, info if world > 1 else None),
            "e2e": {"value": 1.0 / e2e_s, "unit": "matvec/s", "h2d_bytes_per_step": 4 * n,
                    "d2h_bytes_per_step": 4 * n},
            "comm_ms": ph["comm"],
@@ -457,11 +463,13 @@ def main():
     if dist:  # per-rank breakdown (load balance of the domain decomposition)
         mine = {"rank": rank, "n_local": s.n, "phases_ms": ph, "p2p_interactions": int(tm["p2p_interactions"]),
                 "m2l_pairs": int(tm["m2l_pairs"]), "device_mem_used_gb": (total - free) / 1e9, "setup_s": setup_s,
-                "tree_build_ms": tm["tree"], "expansion_slots": int(info["expansion_slots"])}
+                "tree_build_ms": tm["tree"], "expansion_slots": int(info["expansion_slots"]),
+                "gpu_launches": args.steps * launches_per_matvec(info["levels"], P, info)}
         allr = [None] * world
         dist.all_gather_object(allr, mine)
         out["per_rank"] = allr
         out["m2l_pairs"] = int(sum(r["m2l_pairs"] for r in allr))
+        out["gpu_launches"] = int(sum(r["gpu_launches"] for r in allr))  # all ranks' kernels
     if rank == 0 and world == 1 and not args.no_cpu:
         # the oracle as it stands on this host: FP64 direct sums over ALL sources for a seeded sample
         # of rows; the same rows give the full-size parity of the GPU product

@@ -223,6 +223,9 @@ typedef struct {
   double root_origin[3];
   int64_t expansion_slots; /* cells with multipole / local storage on this rank: n_cells on one GPU; the
                               rank's windows + received LET cells with nranks > 1 (FMMBEM_PLAN_CELL_WINDOWS) */
+  int32_t let_send_peers, let_recv_peers; /* nranks > 1: peers this rank sends / receives panel multipoles */
+  int64_t let_cells_sent, let_cells_recv, let_shared_cells; /* per K' matvec (panel LET lists) */
+  int64_t halo_panels_sent, halo_panels_recv;               /* near-field halo weights per matvec */
 } fmmbem_tree_info;
 
 fmmbem_status fmmbem_tree_info_get(const fmmbem_ctx* ctx, fmmbem_tree_info* out);

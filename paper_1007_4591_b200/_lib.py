@@ -56,7 +56,9 @@ class TreeInfo(C.Structure):
     _fields_ = [("levels", C.c_int32), ("n_leaves", C.c_int64), ("n_cells", C.c_int64),
                 ("n_panels", C.c_int64), ("n_charges", C.c_int64), ("nbr_pairs", C.c_int64),
                 ("m2l_pairs", C.c_int64), ("root_width", C.c_double), ("root_origin", C.c_double * 3),
-                ("expansion_slots", C.c_int64)]
+                ("expansion_slots", C.c_int64), ("let_send_peers", C.c_int32), ("let_recv_peers", C.c_int32),
+                ("let_cells_sent", C.c_int64), ("let_cells_recv", C.c_int64), ("let_shared_cells", C.c_int64),
+                ("halo_panels_sent", C.c_int64), ("halo_panels_recv", C.c_int64)]
 
 
 # symbol -> (restype, argtypes); every entry point declared in include/fmmbem.h

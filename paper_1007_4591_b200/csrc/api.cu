@@ -1138,6 +1138,16 @@ fmmbem_status fmmbem_tree_info_get(const fmmbem_ctx* c, fmmbem_tree_info* o) {
   o->root_width = c->tree.W;
   for (int d = 0; d < 3; ++d) o->root_origin[d] = c->tree.x0[d];
   o->expansion_slots = c->n_slots;
+  o->let_send_peers = o->let_recv_peers = 0;
+  for (int p = 0; p < (int)c->let.nsend.size(); ++p) {
+    o->let_send_peers += c->let.nsend[p] > 0;
+    o->let_recv_peers += c->let.nrecv[p] > 0;
+  }
+  o->let_cells_sent = c->let.cells_sent;
+  o->let_cells_recv = c->let.cells_recv;
+  o->let_shared_cells = c->let.nshared;
+  o->halo_panels_sent = c->halo.sent;
+  o->halo_panels_recv = c->halo.recv;
   return FMMBEM_OK;
 }
 
