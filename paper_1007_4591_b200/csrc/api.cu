@@ -854,11 +854,13 @@ fmmbem_status fmmbem_matvec(fmmbem_ctx* c, fmmbem_op op, const float* x, float* 
   API_END
 }
 
-// Host-buffer matvec with the transfers pipelined against the kernels (single GPU, K = 1, no
-// near-field option): x arrives in NCH (default 8) Morton-contiguous chunks on a copy stream and P2M of each
-// chunk's leaves starts as soon as it lands; the far field runs next and L2P writes y first; P2P
-// then adds the near field chunk by chunk and each chunk of y leaves for the host while the next
-// chunk computes.  Same operations as apply_op (P2P and L2P swap order; P2P accumulates).
+// Host-buffer matvec with the transfers pipelined against the kernels (K = 1, no near-field
+// option): x arrives in NCH (default 8) Morton-contiguous chunks of the rank's leaves on a copy
+// stream and P2M of each chunk's leaves starts as soon as it lands; the far field runs next (with
+// several ranks: the LET exchange, then M2L / L2L) and L2P writes y first; the near-field halo is
+// exchanged once x is complete; P2P then adds the near field chunk by chunk and each chunk of y
+// leaves for the host while the next chunk computes.  Same operations as apply_op (P2P and L2P
+// swap order; P2P accumulates).
 void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* yh) {
   constexpr int NCH_MAX = 16;
   static const int NCH = [] {  // transfer chunks (FMMBEM_E2E_CHUNKS, default 8)
@@ -868,7 +870,9 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
   }();
   cudaStream_t st = c->stream;
   const Tree& T = c->tree;
-  const int64_t np = c->np;
+  const bool dist = multi(c);
+  const int64_t own0 = c->pan_lo, n = c->n_own();
+  const int l0 = c->leaf_lo, l1 = c->leaf_hi;
   if (c->h_pan_begin.empty()) {
     c->h_pan_begin.resize(T.n_leaves + 1);
     FMM_CUDA(cudaMemcpy(c->h_pan_begin.data(), c->pan.begin.get(), (T.n_leaves + 1) * sizeof(int),
@@ -878,45 +882,58 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
     FMM_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
     for (auto& e : c->pev) FMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  const auto& hb = c->h_pan_begin;  // local point index of each leaf's first panel
   int lb[NCH_MAX + 1];
-  lb[0] = 0;
+  lb[0] = l0;
   for (int k = 1; k < NCH; ++k) {
-    const int64_t goal = np * k / NCH;
-    lb[k] = (int)(std::lower_bound(c->h_pan_begin.begin(), c->h_pan_begin.end(), (int)goal) - c->h_pan_begin.begin());
-    lb[k] = std::max(lb[k - 1], std::min(lb[k], (int)T.n_leaves));
+    const int64_t goal = own0 + n * k / NCH;
+    lb[k] = (int)(std::lower_bound(hb.begin() + l0, hb.begin() + l1, (int)goal) - hb.begin());
+    lb[k] = std::max(lb[k - 1], std::min(lb[k], l1));
   }
-  lb[NCH] = (int)T.n_leaves;
-  float* x = c->tmp_x.get();
+  lb[NCH] = l1;
+  // x in local point indexing (owned block at own0; with several ranks the halo segments of xext
+  // around it are filled by the halo exchange); y owned-relative
+  float* x = dist ? c->xext.get() : c->tmp_x.get();
   float* y = c->tmp_y.get();
   cudaEvent_t* eh = c->pev;            // x chunk k on the device
   cudaEvent_t* ep = c->pev + NCH_MAX;  // y chunk k final
-  cudaEvent_t e0 = c->pev[2 * NCH_MAX];  // previous work on st done with tmp_x / tmp_y
+  cudaEvent_t e0 = c->pev[2 * NCH_MAX];  // previous work on st done with x / y
   FMM_CUDA(cudaEventRecord(e0, st));
   FMM_CUDA(cudaStreamWaitEvent(c->cstream, e0, 0));
   for (int k = 0; k < NCH; ++k) {
-    const int64_t p0 = c->h_pan_begin[lb[k]], p1 = c->h_pan_begin[lb[k + 1]];
+    const int64_t p0 = hb[lb[k]], p1 = hb[lb[k + 1]];
     if (p1 > p0)
-      FMM_CUDA(cudaMemcpyAsync(x + p0, xh + p0, (p1 - p0) * sizeof(float), cudaMemcpyHostToDevice, c->cstream));
+      FMM_CUDA(cudaMemcpyAsync(x + p0, xh + (p0 - own0), (p1 - p0) * sizeof(float), cudaMemcpyHostToDevice,
+                               c->cstream));
     FMM_CUDA(cudaEventRecord(eh[k], c->cstream));
   }
   SrcArg s;
   s.set = &c->pan;
   s.x = x;
+  const int* tcnt = c->pan.cell_cnt.get();
+  if (dist) {
+    s.leaf_lo = l0;
+    s.leaf_hi = l1;
+    s.cnt = c->pan_own_cnt.get();
+    tcnt = c->pan_own_cnt.get();
+  }
   c->Mx.zero(st);
   for (int k = 0; k < NCH; ++k) {
     FMM_CUDA(cudaStreamWaitEvent(st, eh[k], 0));
     launch_p2m_range(c, s, lb[k], lb[k + 1], st);
   }
   launch_m2m_levels(c, s, st);
-  launch_m2l(c, c->pan.cell_cnt.get(), c->pan.cell_cnt.get(), st);
-  launch_downward(c, c->pan.cell_cnt.get(), st);
-  Outputs o = op_outputs(c, op, x, y);
-  FMM_CUDA(cudaMemsetAsync(y, 0, np * sizeof(float), st));
+  if (dist) exchange_let(c, c->let, st);
+  launch_m2l(c, c->pan.cell_cnt.get(), tcnt, st);
+  launch_downward(c, tcnt, st);
+  Outputs o = op_outputs(c, op, x, y - own0);
+  FMM_CUDA(cudaMemsetAsync(y, 0, std::max<int64_t>(n, 1) * sizeof(float), st));
   TgtArg t = own_targets(c, false);
   Outputs far = o;
   far.pot.x = far.dn.x = nullptr;
   far.pot.d = far.dn.d = nullptr;
   launch_l2p(c, t, far, st);
+  if (dist) halo_exchange(c, x + own0, st);  // the peers' weights for the near field
   o.pot.acc = o.dn.acc = 1;
   if (c->p2p_scaled && op != FMMBEM_OP_SINGLE) s.scaled = prepare_p2p_sources(c, s, st);  // once for all chunks
   for (int k = 0; k < NCH; ++k) {
@@ -926,9 +943,10 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
     launch_p2p(c, tk, s, o, /*self=*/true, /*check=*/false, /*direct=*/false, st);
     FMM_CUDA(cudaEventRecord(ep[k], st));
     FMM_CUDA(cudaStreamWaitEvent(c->cstream, ep[k], 0));
-    const int64_t p0 = c->h_pan_begin[lb[k]], p1 = c->h_pan_begin[lb[k + 1]];
+    const int64_t p0 = hb[lb[k]], p1 = hb[lb[k + 1]];
     if (p1 > p0)
-      FMM_CUDA(cudaMemcpyAsync(yh + p0, y + p0, (p1 - p0) * sizeof(float), cudaMemcpyDeviceToHost, c->cstream));
+      FMM_CUDA(cudaMemcpyAsync(yh + (p0 - own0), y + (p0 - own0), (p1 - p0) * sizeof(float),
+                               cudaMemcpyDeviceToHost, c->cstream));
   }
   FMM_CUDA(cudaStreamSynchronize(c->cstream));
   FMM_CUDA(cudaStreamSynchronize(st));
@@ -946,8 +964,9 @@ fmmbem_status fmmbem_matvec_host(fmmbem_ctx* c, fmmbem_op op, const float* xh, f
   const int64_t n = c->n_own();
   c->tmp_x.alloc(std::max<int64_t>(n, 1));
   c->tmp_y.alloc(std::max<int64_t>(n, 1));
-  const bool pipelined = c->nranks == 1 && c->K == 1 && c->opt.near_mode == 0 && c->opt.direct == 0 &&
-                         c->tree.L >= 2 && op != FMMBEM_OP_DOUBLE && std::getenv("FMMBEM_E2E_PLAIN") == nullptr;
+  const bool pipelined = c->K == 1 && c->opt.near_mode == 0 && c->opt.direct == 0 && c->tree.L >= 2 &&
+                         op != FMMBEM_OP_DOUBLE && (c->nranks == 1 || c->let.ready) &&
+                         std::getenv("FMMBEM_E2E_PLAIN") == nullptr;
   if (pipelined) {
     matvec_host_pipelined(c, op, xh, yh);
     mark_done(c, st);

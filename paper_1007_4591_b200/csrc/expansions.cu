@@ -2,9 +2,9 @@
 // formulas in farfield.cu's header).  One warp per leaf.
 //
 // P2M: lane l owns the sources j = b + l, b + l + 32, ...; the regular solid harmonics of a
-// source are generated one order column m at a time (R_m^m by the diagonal recurrence, then
-// R_n^m = ((2n-1) u_z R_{n-1}^m - r^2 R_{n-2}^m) / ((n-m)(n+m)) with compile-time reciprocals), so
-// only one column of accumulators is live.  Per-lane partial sums go to a private shared-memory
+// source are generated two order columns at a time (R_m^m carried from the previous pass by one
+// diagonal step, then R_n^m = ((2n-1) u_z R_{n-1}^m - r^2 R_{n-2}^m) / ((n-m)(n+m)) with
+// compile-time reciprocals), so only two columns of accumulators are live.  Per-lane partial sums go to a private shared-memory
 // slot and are reduced over lanes (fixed order, no atomics).
 // L2P: lane = target; the leaf's local expansion sits in shared memory (every lane reads the
 // same coefficient -> broadcast); potential and gradient accumulate column by column.
@@ -16,27 +16,15 @@ namespace {
 
 __host__ __device__ constexpr int cx(int n, int m) { return n * (n + 1) / 2 + m; }
 
-constexpr int P2M_TILE = 256;  // sources staged in shared memory per pass (256 measured 3 % faster than 128)
+#ifndef P2M_TILE_N
+#define P2M_TILE_N 128
+#endif
+constexpr int P2M_TILE = P2M_TILE_N;  // sources staged per pass (C5, P = 13: 128 -> 6.30 ms, 256 -> 7.18, 64 -> 8.6)
 
-// R_m^m(u) = (-(x + i y)/2)^m / m!
-template <int m>
-__device__ __forceinline__ void diag(float ux, float uy, float& rr, float& ri) {
-  rr = 1.f;
-  ri = 0.f;
-#pragma unroll
-  for (int k = 1; k <= m; ++k) {
-    const float s = -0.5f / (float)k;
-    const float t = (rr * ux - ri * uy) * s;
-    ri = (rr * uy + ri * ux) * s;
-    rr = t;
-  }
-}
-
-// accumulate column m of w conj(R_n^m(u)), n = m..P-1, into a[] (re, im packed)
+// accumulate column m of w conj(R_n^m(u)), n = m..P-1, into a[] (re, im packed), starting from the
+// column's diagonal R_m^m(u) = (cr, ci)
 template <int P, int m>
-__device__ __forceinline__ void column_acc(float2 (&a)[P - m], float4 u, float r2) {
-  float cr, ci;
-  diag<m>(u.x, u.y, cr, ci);
+__device__ __forceinline__ void column_acc(float2 (&a)[P - m], float4 u, float r2, float cr, float ci) {
   float pr = 0.f, pi = 0.f;
   const float2 nw = make_float2(u.w, -u.w);
   a[0] = __ffma2_rn(nw, make_float2(cr, ci), a[0]);
@@ -53,16 +41,30 @@ __device__ __forceinline__ void column_acc(float2 (&a)[P - m], float4 u, float r
   }
 }
 
-// columns m and P-1-m together (P+1 coefficients, two independent recurrences per source); the
-// lanes' partial sums are transposed through red[P+1][33] and lane c (< P+1) adds the 32 partials of
-// entry c to its register accumulator acc[m] (fixed order, no atomics).  Odd P: the middle column
-// m = (P-1)/2 is reduced alone (P - m coefficients).
+// R_{k+1}^{k+1} = R_k^k (-(x + i y) / 2) / (k + 1)
+template <int k>
+__device__ __forceinline__ void diag_step(float ux, float uy, float& rr, float& ri) {
+  constexpr float s = -0.5f / (float)(k + 1);
+  const float t = (rr * ux - ri * uy) * s;
+  ri = (rr * uy + ri * ux) * s;
+  rr = t;
+}
+
+__host__ __device__ constexpr int p2m_half(int P) { return (P + 1) / 2; }
+
+// Pass m: columns m and m2 = m + H (H = ceil(P/2); the last pass of odd P has column m alone).
+// Each source's two diagonals R_m^m, R_m2^m2 live in the lane-private shared slot dg[j] and
+// advance by one order per pass (one complex multiply each instead of recomputing m steps).  The
+// lanes' partial sums are transposed through red[][33] and lane c (< entries) adds the 32 partials
+// of entry c to its register accumulator acc[m] (fixed order, no atomics).
 template <int P, int m>
-__device__ __forceinline__ void p2m_columns(float2 (&acc)[(P + 1) / 2], float2* red, const float4* src, int ns,
-                                            int lane) {
-  constexpr int m2 = P - 1 - m;
-  constexpr bool single = (m == m2);
+__device__ __forceinline__ void p2m_columns(float2 (&acc)[p2m_half(P)], float2* red, const float4* src, float4* dg,
+                                            int ns, int lane) {
+  constexpr int H = p2m_half(P);
+  constexpr int m2 = m + H;
+  constexpr bool single = m2 >= P;
   constexpr int NB = single ? 1 : P - m2;
+  constexpr bool last = (m + 1 == H);
   float2 a[P - m], b[NB];
 #pragma unroll
   for (int k = 0; k < P - m; ++k) a[k] = make_float2(0.f, 0.f);
@@ -70,9 +72,15 @@ __device__ __forceinline__ void p2m_columns(float2 (&acc)[(P + 1) / 2], float2* 
   for (int k = 0; k < NB; ++k) b[k] = make_float2(0.f, 0.f);
   for (int j = lane; j < ns; j += 32) {
     const float4 u = src[j];
+    float4 d = dg[j];
     const float r2 = fmaf(u.x, u.x, fmaf(u.y, u.y, u.z * u.z));
-    column_acc<P, m>(a, u, r2);
-    if constexpr (!single) column_acc<P, m2>(b, u, r2);
+    column_acc<P, m>(a, u, r2, d.x, d.y);
+    if constexpr (!single) column_acc<P, (single ? m : m2)>(b, u, r2, d.z, d.w);
+    if constexpr (!last) {
+      diag_step<m>(u.x, u.y, d.x, d.y);
+      if constexpr (!single && m2 + 1 < P) diag_step<(single ? m : m2)>(u.x, u.y, d.z, d.w);
+      dg[j] = d;
+    }
   }
 #pragma unroll
   for (int k = 0; k < P - m; ++k) red[k * 33 + lane] = a[k];
@@ -81,7 +89,7 @@ __device__ __forceinline__ void p2m_columns(float2 (&acc)[(P + 1) / 2], float2* 
     for (int k = 0; k < P - m2; ++k) red[(P - m + k) * 33 + lane] = b[k];
   }
   __syncwarp();
-  constexpr int NE = single ? P - m : P + 1;
+  constexpr int NE = single ? P - m : 2 * P - m - m2;
   if (lane < NE) {
     float2 s0 = make_float2(0.f, 0.f), s1 = s0;
 #pragma unroll
@@ -92,48 +100,61 @@ __device__ __forceinline__ void p2m_columns(float2 (&acc)[(P + 1) / 2], float2* 
     acc[m] = __fadd2_rn(acc[m], __fadd2_rn(s0, s1));
   }
   __syncwarp();
-  if constexpr (m + 1 <= P - 2 - m) p2m_columns<P, m + 1>(acc, red, src, ns, lane);
+  if constexpr (!last) p2m_columns<P, m + 1>(acc, red, src, dg, ns, lane);
 }
 
 // P2M, one warp per leaf: the leaf's sources are scaled into the cell frame and staged in shared
-// memory once (u = (y - c)/w, weight), then every lane accumulates its sources' columns in
-// registers (two columns at a time for ILP) and the column pair is reduced over the lanes at once,
-// so shared memory stays small (occupancy) whatever P.
+// memory once (u = (y - c)/w, weight) with their starting diagonals (R_0^0 = 1, R_H^H), then every
+// lane accumulates its sources' columns in registers (two columns at a time for ILP) and the column
+// pair is reduced over the lanes at once, so shared memory stays small (occupancy) whatever P.
 template <int P>
 __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
                                               const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               float2* __restrict__ M) {
   constexpr int NC = P * (P + 1) / 2;
-  constexpr int NPAIR = (P + 1) / 2;  // column pairs (m, P-1-m); odd P: the last one is the middle column
-  __shared__ float2 red[(P + 1) * 33];
+  constexpr int H = p2m_half(P);  // passes: columns (m, m + H)
+  constexpr int NEMAX = 2 * P - H;
+  __shared__ float2 red[NEMAX * 33];
   __shared__ float4 src[P2M_TILE];
+  __shared__ float4 dg[P2M_TILE];
   const int leaf = leaf0 + blockIdx.x;
   const int b = beg[leaf], e = beg[leaf + 1];
   if (b == e) return;
   const int lane = threadIdx.x;
-  float2 acc[NPAIR];
+  float2 acc[H];
 #pragma unroll
-  for (int k = 0; k < NPAIR; ++k) acc[k] = make_float2(0.f, 0.f);
+  for (int k = 0; k < H; ++k) acc[k] = make_float2(0.f, 0.f);
   for (int t0 = b; t0 < e; t0 += P2M_TILE) {
     const int ns = min(P2M_TILE, e - t0);
     __syncwarp();
-    for (int k = lane; k < ns; k += 32) {
+    for (int k = lane; k < ns; k += 32) {  // lane k % 32 stages exactly the sources it accumulates
       const int j = t0 + k;
       const float4 p = __ldg(pos + j);
       float w = p.w;
       if (x) w *= __ldg(x + (div == 1 ? j : j / div));
-      src[k] = make_float4(p.x * inv_w, p.y * inv_w, p.z * inv_w, w);
+      const float ux = p.x * inv_w, uy = p.y * inv_w;
+      src[k] = make_float4(ux, uy, p.z * inv_w, w);
+      float hr = 1.f, hi = 0.f;  // R_H^H
+#pragma unroll
+      for (int q = 1; q <= H; ++q) {
+        const float sc = -0.5f / (float)q;
+        const float t = (hr * ux - hi * uy) * sc;
+        hi = (hr * uy + hi * ux) * sc;
+        hr = t;
+      }
+      dg[k] = make_float4(1.f, 0.f, hr, hi);
     }
     __syncwarp();
-    p2m_columns<P, 0>(acc, red, src, ns, lane);
+    p2m_columns<P, 0>(acc, red, src, dg, ns, lane);
   }
-  if (lane < P + 1) {
+  if (lane < NEMAX) {
     float2* Mo = M + (size_t)(leaf_off + leaf) * NC;
 #pragma unroll
-    for (int m = 0; m < NPAIR; ++m) {
-      const int m2 = P - 1 - m;
+    for (int m = 0; m < H; ++m) {
+      const int m2 = m + H;
+      const int ne = m2 < P ? 2 * P - m - m2 : P - m;
+      if (lane >= ne) continue;
       // entry lane: (n = m + lane, m) for lane < P - m, else (n = m2 + lane - (P - m), m2)
-      if (m == m2 && lane >= P - m) continue;  // odd P: the middle column has P - m entries
       const int n = lane < P - m ? m + lane : m2 + lane - (P - m);
       const int mm = lane < P - m ? m : m2;
       Mo[cx(n, mm)] = acc[m];

@@ -35,7 +35,9 @@ def test_two_gpus_match_one(case):
             assert m["n_local"] > 0
             assert m["matvec_rel"] < 1e-6, m
             assert m["double_rel"] < 1e-6, m
-            assert m["host_rel"] == 0.0, m  # host-buffer product = device product (same path on N > 1)
+            # host-buffer product (pipelined: L2P before the chunked P2P) = device product up to
+            # the order of the near + far addition
+            assert m["host_rel"] < 1e-6, m
             g, o, gi, oi = m["solve"]
             assert abs(g / o - 1) < 1e-6 and abs(gi - oi) <= 1, m
             assert abs(m["bibee"][0] / m["bibee"][1] - 1) < 1e-6, m

@@ -75,7 +75,7 @@ def main():
         sig = gather(s, r["sigma"])
         phi = s.reaction_potential(torch.tensor(sig[s.local_ids], dtype=torch.float32, device="cuda"))
         res[f"mode{mode}"] = dict(n_local=s.n, matvec_rel=rel(y, y1), double_rel=rel(yd, yd1),
-                                  host_rel=float(np.abs(yh - y[s.local_ids]).max()),
+                                  host_rel=rel(yh, y[s.local_ids]),
                                   solve=(r["dG"], r1["dG"], r["iterations"], r1["iterations"]),
                                   bibee=(b["dG"], b1["dG"]), phi_rel=rel(phi, phi1),
                                   slots=s.tree_info()["expansion_slots"], n_cells=s.tree_info()["n_cells"])
