@@ -90,6 +90,11 @@ typedef struct {
                             r's triangle k is k + (triangles of ranks < r) -- memory O(N/R) per rank (SURVEY
                             8(e)); near_mode and self_term need mode 0.  Either way the panels move to the rank
                             owning their leaf; default 0 */
+  int32_t charge_terms;  /* expansion order of the charge-FMM (E_n and psi from the charges; the
+                            BIBEE energy and the GMRES right-hand side): 0 = terms (default); else one of the
+                            rotation orders 8, 10, 12, 13, 14 and <= terms.  The charges sit >= 1.4 A inside the
+                            surface, so their fields converge faster in P than a random-x K' product; the
+                            bench's parity rows report the E_n / psi error at the order used */
 } fmmbem_options;
 
 /* FMMBEM_ABI_VERSION of the built library; sizes of the ABI structs (bindings check these). */

@@ -33,7 +33,7 @@ class Options(C.Structure):
                 ("quad_points", C.c_int32), ("near_mode", C.c_int32), ("near_radius", C.c_float),
                 ("self_term", C.c_int32), ("direct", C.c_int32), ("deterministic", C.c_int32),
                 ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("nccl_id", C.c_void_p), ("input_mode", C.c_int32)]
+                ("nccl_id", C.c_void_p), ("input_mode", C.c_int32), ("charge_terms", C.c_int32)]
 
 
 class SolveOptions(C.Structure):

@@ -417,6 +417,20 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
     o.pot.y = c->psi.get() - c->pan_lo;
     o.pot.b = (float)(1.0 / FOUR_PI);
   }
+  // the charge-FMM runs at its own order (options.charge_terms): every far-field launcher reads
+  // c->P / c->NC, and the expansion / LET buffers are sized for terms >= charge_terms
+  struct OrderScope {
+    fmmbem_ctx* c;
+    int P0, NC0;
+    OrderScope(fmmbem_ctx* c_, int P) : c(c_), P0(c_->P), NC0(c_->NC) {
+      c->P = P;
+      c->NC = P * (P + 1) / 2;
+    }
+    ~OrderScope() {
+      c->P = P0;
+      c->NC = NC0;
+    }
+  } order(c, c->P_chg);
   // phase events of this charge-FMM (fmmbem_last_timing reports them until the next matvec)
   if (c->p2p_inter_chg < 0 && c->tree.L >= 2 && !c->opt.direct)
     c->p2p_inter_chg = count_p2p(c, c->pan, c->chg, false, false, c->leaf_lo, c->leaf_hi);
@@ -540,6 +554,7 @@ fmmbem_status fmmbem_default_options(fmmbem_options* o) {
   o->nranks = 1;
   o->nccl_id = nullptr;
   o->input_mode = 0;
+  o->charge_terms = 0;
   return FMMBEM_OK;
 }
 
@@ -567,6 +582,8 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   if (opt.nranks > 1 && !opt.nccl_id) throw Error(FMMBEM_E_INVALID, "nranks > 1 needs options.nccl_id");
   if (opt.nranks > 1 && opt.direct) throw Error(FMMBEM_E_INVALID, "direct mode is single-GPU only");
   if (opt.input_mode != 0 && opt.input_mode != 1) throw Error(FMMBEM_E_INVALID, "input_mode must be 0 or 1");
+  if (opt.charge_terms != 0 && (!rot_supported(opt.charge_terms) || opt.charge_terms > opt.terms))
+    throw Error(FMMBEM_E_INVALID, "charge_terms must be 0 or one of 8, 10, 12, 13, 14 and <= terms");
   const bool parts = opt.nranks > 1 && opt.input_mode == 1;
   if (parts && (opt.near_mode || opt.self_term))
     throw Error(FMMBEM_E_INVALID, "near_mode / self_term need the full mesh on every rank (input_mode 0)");
@@ -611,6 +628,12 @@ fmmbem_status fmmbem_create(const fmmbem_mesh* mesh, const fmmbem_charges* chg, 
   c->overlap = opt.nranks > 1 ? 1 : 0;
   if (const char* e = std::getenv("FMMBEM_OVERLAP")) c->overlap = std::atoi(e);
   c->NC = c->P * (c->P + 1) / 2;
+  c->P_chg = opt.charge_terms ? opt.charge_terms : c->P;
+  if (const char* e = std::getenv("FMMBEM_CHARGE_TERMS")) {  // A/B knob (same rules as the option)
+    const int v = std::atoi(e);
+    if (rot_supported(v) && v <= c->P) c->P_chg = v;
+  }
+  if (c->m2l_mode != 0) c->P_chg = c->P;  // the O(P^4) tables are built for terms only
   c->K = opt.quad_points;
   c->eps_in = eps_in;
   c->eps_out = eps_out;

@@ -102,6 +102,7 @@ struct HaloPlan {
 struct fmmbem_ctx {
   fmmbem_options opt{};
   int P = 10, K = 1, NC = 55;  // terms, quadrature points, complex coefficients per expansion
+  int P_chg = 10;              // order of the charge-FMM (options.charge_terms; ensure_fields swaps it in)
   double eps_in = 4, eps_out = 80, f = 0, eps_hat = 0;
   int64_t np = 0, nc = 0;  // panels of ALL ranks, charges (replicated)
   int device = 0;

@@ -3,14 +3,14 @@ order P given, time the A = I - f K' matvec (CUDA events, 10 steps) and check K'
 sample of rows against the FP64 oracle for a random x, the per-molecule E_n field (the physical
 GMRES right-hand side, tiled over the 1000 copies) and x = 1.
 
-  python tools/c5_probe.py 12 13 14      (PROBE_ROWS = sampled rows, default 1024)
+  python tests/probes/c5_probe.py 12 13 14      (PROBE_ROWS = sampled rows, default 1024)
 """
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 

@@ -1,6 +1,6 @@
 """Developer check: print parity numbers of the CUDA path vs the oracle (not a test)."""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 from paper_1007_4591_b200 import Solver
