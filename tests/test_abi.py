@@ -52,6 +52,18 @@ def test_create_rejects_bad_input_without_touching_gpu(lib):
     assert h.value is None
     assert b"null" in lib.fmmbem_last_error()
     lib.fmmbem_destroy(None)  # NULL-safe
+    # option validation happens before any CUDA call: charge_terms must be 0 or a rotation order <= terms
+    import numpy as np
+    v = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], np.float64)
+    t = np.array([[0, 2, 1], [0, 1, 3], [0, 3, 2], [1, 2, 3]], np.int32)
+    mesh = _lib.Mesh(len(v), v.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(t),
+                     t.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    for ct, terms in ((11, 13), (14, 13), (-1, 13), (9, 10)):
+        o = _lib.Options()
+        lib.fmmbem_default_options(ctypes.byref(o))
+        o.terms, o.charge_terms = terms, ct
+        assert lib.fmmbem_create(ctypes.byref(mesh), None, 4.0, 80.0, ctypes.byref(o), ctypes.byref(h)) == _lib.E_INVALID
+        assert b"charge_terms" in lib.fmmbem_last_error()
 
 
 def test_sm100a_code_in_library():

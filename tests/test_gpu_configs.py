@@ -141,3 +141,24 @@ def test_c5_array_sampled_rows():
             assert np.isfinite(y).all()
             assert np.array_equal(y, matvec_global(s, x, "kprime"))
     assert all(l2 < 1e-4 and mx < 1e-3 for l2, mx in errs.values()), errs
+
+
+def test_charge_terms_fields_energy_and_matvec_unchanged():
+    """options.charge_terms (the charge-FMM order, the bench uses 12 under K' order 13): on C3 the
+    fields E_n / psi stay within 1e-4 of the oracle at 12 (measured 3.3e-5 / 1.8e-6) and the BIBEE
+    energy within 1e-3 at 10 and 12 (measured 2e-6 / 7e-7); the K' matvec does not depend on it."""
+    cfg = configs.lysozyme(113)
+    P = bem.Problem(cfg)
+    psi_ref = bem.charge_potential(P.pan, cfg["charge_xyz"], cfg["charge_q"])
+    e_ref = P.bibee("cfa")["dG"]
+    x = np.random.default_rng(5).normal(size=P.pan.n)
+    y13 = matvec_global(solver(cfg, **BENCH), x, "kprime")
+    for ct in (12, 10):
+        s = solver(cfg, charge_terms=ct, **BENCH)
+        assert np.array_equal(matvec_global(s, x, "kprime"), y13)
+        En, psi = s.charge_fields()
+        En = s.to_global(En.cpu().numpy().astype(np.float64))
+        psi = s.to_global(psi.cpu().numpy().astype(np.float64))
+        if ct == 12:
+            assert bem.rel_l2(En, P.E) < 1e-4 and bem.rel_l2(psi, psi_ref) < 1e-4
+        assert abs(s.bibee("cfa")["dG"] / e_ref - 1) < 1e-3
