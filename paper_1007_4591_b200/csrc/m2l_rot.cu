@@ -127,6 +127,23 @@ struct Slot {
   __device__ __forceinline__ void set(int c, float2 v) const { base[c * 33] = v; }
 };
 
+// The M2L slot with its last NREG coefficients in registers: the shared-memory part shrinks to
+// (NC - NREG) x 33 float2 per warp, which is what bounds the lockstep kernel's resident warps
+// (P = 13: 88 instead of 91 rows -> 10 warps per SM instead of 9).  Every index is a compile-time
+// constant after unrolling, so the register entries never spill to local memory.
+template <int NC, int NREG>
+struct SlotR {
+  static constexpr int C0 = NC - NREG;  // first register entry
+  float2* base;
+  float2 r[NREG > 0 ? NREG : 1];
+  __device__ __forceinline__ float2 get(int c) const { return (NREG > 0 && c >= C0) ? r[c - C0] : base[c * 33]; }
+  __device__ __forceinline__ void set(int c, float2 v) {
+    if (NREG > 0 && c >= C0) r[c - C0] = v;
+    else base[c * 33] = v;
+  }
+  __device__ __forceinline__ void set(int c, float re, float im) { set(c, make_float2(re, im)); }
+};
+
 __device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
 
 // one degree block: b = X a (E/F form), a and b in registers
@@ -156,8 +173,8 @@ __device__ __forceinline__ void cmul_ip(float& r, float& s, float zr, float zi) 
 }
 
 // M' block n = rho^-n D Phi(t) D^-1 Phi(p + pi/2) M_n
-template <int P, int n>
-__device__ __forceinline__ void pass_a(const Slot& sl, const float2* __restrict__ Ms, const float (&zar)[P],
+template <int P, int n, class S>
+__device__ __forceinline__ void pass_a(S& sl, const float2* __restrict__ Ms, const float (&zar)[P],
                                        const float (&zai)[P], const float (&zbr)[P], const float (&zbi)[P],
                                        float scale, float irho) {
   constexpr int c0 = n * (n + 1) / 2;
@@ -176,12 +193,12 @@ __device__ __forceinline__ void pass_a(const Slot& sl, const float2* __restrict_
   mat_block<n, 1>(br, bi, ar, ai);                    // D
 #pragma unroll
   for (int m = 0; m <= n; ++m) sl.set(c0 + m, __fmul2_rn(make_float2(ar[m], ai[m]), bc2(scale)));
-  if constexpr (n + 1 < P) pass_a<P, n + 1>(sl, Ms, zar, zai, zbr, zbi, scale * irho, irho);
+  if constexpr (n + 1 < P) pass_a<P, n + 1, S>(sl, Ms, zar, zai, zbr, zbi, scale * irho, irho);
 }
 
 // coaxial translation of order column k (input scaled by rho^-n, output missing rho^-(j+1))
-template <int P, int k>
-__device__ __forceinline__ void pass_b(const Slot& sl) {
+template <int P, int k, class S>
+__device__ __forceinline__ void pass_b(S& sl) {
   asm volatile("" ::: "memory");
   float2 t[P - k];
 #pragma unroll
@@ -194,12 +211,12 @@ __device__ __forceinline__ void pass_b(const Slot& sl) {
     for (int n = k; n < P; ++n) acc = __ffma2_rn(bc2(sg * factf(j + n)), t[n - k], acc);  // packed re/im
     sl.set(j * (j + 1) / 2 + k, acc);
   }
-  if constexpr (k + 1 < P) pass_b<P, k + 1>(sl);
+  if constexpr (k + 1 < P) pass_b<P, k + 1, S>(sl);
 }
 
 // L block j = Phi(-p - pi/2) D^-T Phi(-t) D^T rho^-(j+1) L'_j
-template <int P, int n>
-__device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], const float (&zai)[P],
+template <int P, int n, class S>
+__device__ __forceinline__ void pass_c(S& sl, const float (&zar)[P], const float (&zai)[P],
                                        const float (&zbr)[P], const float (&zbi)[P], float scale, float irho) {
   constexpr int c0 = n * (n + 1) / 2;
   asm volatile("" ::: "memory");
@@ -219,12 +236,12 @@ __device__ __forceinline__ void pass_c(const Slot& sl, const float (&zar)[P], co
     if (m > 0) cmul_ip(ar[m], ai[m], zar[m], -zai[m]);  // Phi(-p - pi/2)
     sl.set(c0 + m, ar[m], ai[m]);
   }
-  if constexpr (n + 1 < P) pass_c<P, n + 1>(sl, zar, zai, zbr, zbi, scale * irho, irho);
+  if constexpr (n + 1 < P) pass_c<P, n + 1, S>(sl, zar, zai, zbr, zbi, scale * irho, irho);
 }
 
 // the translated local expansion of source cell s at target (tx, ty, tz) into the thread's slot
-template <int P>
-__device__ __forceinline__ void translate_pair(const Slot& sl, int tx, int ty, int tz, int s,
+template <int P, class S>
+__device__ __forceinline__ void translate_pair(S& sl, int tx, int ty, int tz, int s,
                                                const uint64_t* __restrict__ key, const float2* __restrict__ M) {
   constexpr int NC = P * (P + 1) / 2;
   int sx, sy, sz;
@@ -252,15 +269,15 @@ __device__ __forceinline__ void translate_pair(const Slot& sl, int tx, int ty, i
     zbr[m] = zbr[m - 1] * br1 - zbi[m - 1] * bi1;
     zbi[m] = zbr[m - 1] * bi1 + zbi[m - 1] * br1;
   }
-  pass_a<P, 0>(sl, M + (size_t)s * NC, zar, zai, zbr, zbi, 1.f, irho);
-  pass_b<P, 0>(sl);
-  pass_c<P, 0>(sl, zar, zai, zbr, zbi, irho, irho);
+  pass_a<P, 0, S>(sl, M + (size_t)s * NC, zar, zai, zbr, zbi, 1.f, irho);
+  pass_b<P, 0, S>(sl);
+  pass_c<P, 0, S>(sl, zar, zai, zbr, zbi, irho, irho);
 }
 
 // Lockstep variant: the W warps of a CTA (one target row each) start every 32-pair round together
 // (__syncthreads per round), so the SM's warps walk the long unrolled body in step and share the
 // instruction-cache lines (the body is ~3x the L1.5 I$); dynamic shared memory, W slots.
-template <int P, int W, int RPW>
+template <int P, int W, int RPW, int NREG>
 __global__ void __launch_bounds__(32 * W) k_m2l_rot_sync(int rows, const int* __restrict__ tcells,
                                                          const int* __restrict__ off, const int* __restrict__ idx,
                                                          const uint64_t* __restrict__ key,
@@ -271,13 +288,15 @@ __global__ void __launch_bounds__(32 * W) k_m2l_rot_sync(int rows, const int* __
   // order), so the result does not depend on which warp that is.
   constexpr int NC = P * (P + 1) / 2;
   constexpr int NR = (NC + 31) / 32;
+  constexpr int NS = NC - NREG;  // shared-memory rows of the slot
   extern __shared__ float2 svdyn[];
   __shared__ int next_row;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r_beg = blockIdx.x * W * RPW, r_end = min(rows, r_beg + W * RPW);
   if (threadIdx.x == 0) next_row = r_beg + W;
-  float2* sv = svdyn + (size_t)w * NC * 33;
-  const Slot sl{sv + lane};
+  float2* sv = svdyn + (size_t)w * NS * 33;
+  SlotR<NC, NREG> sl;
+  sl.base = sv + lane;
   int row = r_beg + w;
   int cell = 0, lo = 0, hi = 0, e0 = 0, tx = 0, ty = 0, tz = 0;
   auto start = [&]() {
@@ -305,15 +324,30 @@ __global__ void __launch_bounds__(32 * W) k_m2l_rot_sync(int rows, const int* __
 #pragma unroll
         for (int c = 0; c < NC; ++c) sl.set(c, 0.f, 0.f);
       }
+      // the register rows: butterfly sums over the 32 pairs (fixed order)
+      float2 rs[NREG > 0 ? NREG : 1];
+#pragma unroll
+      for (int q = 0; q < NREG; ++q) {
+        rs[q] = sl.r[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          rs[q].x += __shfl_xor_sync(0xffffffffu, rs[q].x, o);
+          rs[q].y += __shfl_xor_sync(0xffffffffu, rs[q].y, o);
+        }
+      }
       __syncwarp();
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         const int c = lane + 32 * r;
-        if (c < NC) {
+        if (c < NS) {
           float2 sum = make_float2(0.f, 0.f);
 #pragma unroll 8
           for (int l = 0; l < 32; ++l) sum = __fadd2_rn(sum, sv[c * 33 + l]);
           acc[r] = __fadd2_rn(acc[r], sum);
+        } else if (c < NC) {
+#pragma unroll
+          for (int q = 0; q < NREG; ++q)
+            if (c == NS + q) acc[r] = __fadd2_rn(acc[r], rs[q]);
         }
       }
       __syncwarp();
@@ -801,23 +835,37 @@ void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st) {
 #ifndef M2L_RPW
 #define M2L_RPW 16  // rows per warp in a CTA's Morton window
 #endif
-template <int P, int W>
+template <int P, int W, int NREG>
 void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem, cudaStream_t st) {
   static unsigned long long attr_devices = 0;  // the attribute is per device: set it once on each
   int dev = 0;
   FMM_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !(attr_devices >> dev & 1ULL)) {
-    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W, M2L_RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot_sync<P, W, M2L_RPW, NREG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     attr_devices |= 1ULL << dev;
   }
-  k_m2l_rot_sync<P, W, M2L_RPW><<<ceil_div(w.rows, M2L_RPW * W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
+  k_m2l_rot_sync<P, W, M2L_RPW, NREG><<<ceil_div(w.rows, M2L_RPW * W), 32 * W, smem, st>>>((int)w.rows, w.cell.get(), w.off.get(),
                                                                    w.idx.get(), c->slot_keys(), c->Mx.get(),
                                                                    c->Lx.get());
 }
 
-// lockstep warps per CTA: as many per-warp slots (NC x 33 float2) as fit the SM's 227 KB of shared
-// memory -- one CTA per SM (P = 12: 11 warps, 13: 9, 14: 8)
-constexpr int m2l_warps(int P) { return (227 * 1024) / ((P * (P + 1) / 2) * 33 * 8); }
+// lockstep warps per CTA: as many per-warp slots ((NC - NREG) x 33 float2) as fit the SM's 227 KB of
+// shared memory -- one CTA per SM.  NREG = the slot rows kept in registers: the fewest that gain
+// one more warp (P = 13: 3 -> 10 warps instead of 9); 0 where that costs more than 4 rows or the
+// CTA would exceed 16 warps (< 128 registers per thread: the low orders then spill).
+#ifndef M2L_NREG_MAX
+#define M2L_NREG_MAX 4
+#endif
+constexpr int m2l_nc(int P) { return P * (P + 1) / 2; }
+constexpr int m2l_warps_for(int P, int nreg) { return (227 * 1024) / ((m2l_nc(P) - nreg) * 33 * 8); }
+constexpr int m2l_nreg(int P) {
+  const int w0 = m2l_warps_for(P, 0);
+  for (int k = 1; k <= M2L_NREG_MAX; ++k)
+    if (m2l_warps_for(P, k) > w0) return m2l_warps_for(P, k) <= 16 ? k : 0;
+  return 0;
+}
+constexpr int m2l_warps(int P) { return m2l_warps_for(P, m2l_nreg(P)); }
 
 void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
   if (w.rows == 0) return;
@@ -830,8 +878,8 @@ void launch_m2l_rot(fmmbem_ctx* c, const M2LWork& w, cudaStream_t st) {
 #define FMM_ROT_CASE(PP)                                                                                   \
   case PP:                                                                                                 \
     if (!indep) {                                                                                          \
-      constexpr int W = m2l_warps(PP);                                                                     \
-      m2l_sync_launch<PP, W>(w, T, c, (size_t)W * (PP * (PP + 1) / 2) * 33 * sizeof(float2), st);        \
+      constexpr int W = m2l_warps(PP), NREG = m2l_nreg(PP);                                               \
+      m2l_sync_launch<PP, W, NREG>(w, T, c, (size_t)W * (m2l_nc(PP) - NREG) * 33 * sizeof(float2), st);   \
     } else {                                                                                               \
       k_m2l_rot<PP, 1><<<(int)w.rows, 32, 0, st>>>((int)w.rows, w.cell.get(), w.off.get(), w.idx.get(),   \
                                                    c->slot_keys(), c->Mx.get(), c->Lx.get());              \
