@@ -851,17 +851,19 @@ void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem
 }
 
 // lockstep warps per CTA: as many per-warp slots ((NC - NREG) x 33 float2) as fit the SM's 227 KB of
-// shared memory -- one CTA per SM.  NREG = the slot rows kept in registers: the fewest that gain
-// one more warp (P = 13: 3 -> 10 warps instead of 9); 0 where that costs more than 4 rows or the
-// CTA would exceed 16 warps (< 128 registers per thread: the low orders then spill).
-#ifndef M2L_NREG_MAX
-#define M2L_NREG_MAX 4
+// shared memory -- one CTA per SM.  NREG = the slot rows kept in registers.  P = 13 (the bench
+// order): 11 rows -> 11 warps instead of 9, 168 registers, no spills (C5: M2L 36.6 -> 33.2 ms; 3 rows
+// / 10 warps: 35.3 ms).  Other orders: the fewest rows (<= 4) that gain one warp while the CTA stays
+// <= 16 warps (>= 128 registers per thread), else none.
+#ifndef M2L_NREG13
+#define M2L_NREG13 11
 #endif
 constexpr int m2l_nc(int P) { return P * (P + 1) / 2; }
 constexpr int m2l_warps_for(int P, int nreg) { return (227 * 1024) / ((m2l_nc(P) - nreg) * 33 * 8); }
 constexpr int m2l_nreg(int P) {
+  if (P == 13) return M2L_NREG13;
   const int w0 = m2l_warps_for(P, 0);
-  for (int k = 1; k <= M2L_NREG_MAX; ++k)
+  for (int k = 1; k <= 4; ++k)
     if (m2l_warps_for(P, k) > w0) return m2l_warps_for(P, k) <= 16 ? k : 0;
   return 0;
 }
