@@ -61,7 +61,8 @@ struct P2PItems {
 // analytic near-field correction (near_mode = 1): CSR over this rank's target rows
 struct NearCSR {
   int64_t nnz = 0;
-  DevBuf<int> off, col;
+  DevBuf<long long> off;  // 64-bit: ~28 pairs per panel exceed 2^31 entries at C5
+  DevBuf<int> col;
   DevBuf<float> vkp, vsl, diag;
 };
 

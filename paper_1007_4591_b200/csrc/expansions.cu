@@ -170,6 +170,9 @@ __global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, co
 // so that per target and coefficient (cr + i ci) = R_n^m(u) the update is
 //   (gx, gy) += (X.re, Y.re) cr + (X.im, Y.im) ci,  (gz, ph) += (Z.re, Phi.re) cr + (Z.im, Phi.im) ci
 // -- four packed FP32x2 FMAs; the recurrence for R_n^m is packed over (re, im) as well.
+#ifndef L2P_NT
+#define L2P_NT 1
+#endif
 template <int P, bool POT, bool DN>
 __global__ void __launch_bounds__(32) k_l2p_t(const float4* __restrict__ pos, const float4* __restrict__ nrm,
                                               const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
@@ -210,48 +213,79 @@ __global__ void __launch_bounds__(32) k_l2p_t(const float4* __restrict__ pos, co
     zph[c] = z;
   }
   __syncwarp();
-  for (int i = b + lane; i < e; i += 32) {
-    const float4 p = pos[i];
-    const float ux = p.x * inv_w, uy = p.y * inv_w, uz = p.z * inv_w;
-    const float r2 = fmaf(ux, ux, fmaf(uy, uy, uz * uz));
-    float2 gxy2 = make_float2(0.f, 0.f), gzph = make_float2(0.f, 0.f);
-    float dr = 1.f, di = 0.f;
+  // NT targets per lane (L2P_NT, default 1): the table reads are shared by the lane's targets
+  constexpr int NT = L2P_NT;
+  for (int i0 = b + lane; i0 < e; i0 += 32 * NT) {
+    float ux[NT], uy[NT], uz[NT], r2[NT], dr[NT], di[NT];
+    float2 gxy2[NT], gzph[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const int i = min(i0 + 32 * q, e - 1);
+      const float4 p = pos[i];
+      ux[q] = p.x * inv_w;
+      uy[q] = p.y * inv_w;
+      uz[q] = p.z * inv_w;
+      r2[q] = fmaf(ux[q], ux[q], fmaf(uy[q], uy[q], uz[q] * uz[q]));
+      gxy2[q] = make_float2(0.f, 0.f);
+      gzph[q] = make_float2(0.f, 0.f);
+      dr[q] = 1.f;
+      di[q] = 0.f;
+    }
 #pragma unroll
     for (int m = 0; m < P; ++m) {
       asm volatile("" ::: "memory");  // re-read the tables per column (no hoisting over the target loop)
-      if (m > 0) {
-        const float s = -0.5f / (float)m;
-        const float t = (dr * ux - di * uy) * s;
-        di = (dr * uy + di * ux) * s;
-        dr = t;
+      float2 cur[NT], prev[NT];
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        if (m > 0) {
+          const float s = -0.5f / (float)m;
+          const float t = (dr[q] * ux[q] - di[q] * uy[q]) * s;
+          di[q] = (dr[q] * uy[q] + di[q] * ux[q]) * s;
+          dr[q] = t;
+        }
+        cur[q] = make_float2(dr[q], di[q]);
+        prev[q] = make_float2(0.f, 0.f);
       }
-      float2 cur = make_float2(dr, di), prev = make_float2(0.f, 0.f);
 #pragma unroll
       for (int n = m; n < P; ++n) {
         if (n > m) {
           const float inv = 1.f / (float)((n - m) * (n + m));
-          const float a = (float)(2 * n - 1) * inv * uz, bb = r2 * inv;
-          const float2 nxt = __ffma2_rn(make_float2(a, a), cur, __fmul2_rn(make_float2(-bb, -bb), prev));
-          prev = cur;
-          cur = nxt;
+#pragma unroll
+          for (int q = 0; q < NT; ++q) {
+            const float a = (float)(2 * n - 1) * inv * uz[q], bb = r2[q] * inv;
+            const float2 nxt = __ffma2_rn(make_float2(a, a), cur[q], __fmul2_rn(make_float2(-bb, -bb), prev[q]));
+            prev[q] = cur[q];
+            cur[q] = nxt;
+          }
         }
         const int c = cx(n, m);
         if (DN && n + 1 < P) {
           const float4 g = gxy[c];
-          gxy2 = __ffma2_rn(make_float2(g.x, g.y), make_float2(cur.x, cur.x), gxy2);
-          gxy2 = __ffma2_rn(make_float2(g.z, g.w), make_float2(cur.y, cur.y), gxy2);
+#pragma unroll
+          for (int q = 0; q < NT; ++q) {
+            gxy2[q] = __ffma2_rn(make_float2(g.x, g.y), make_float2(cur[q].x, cur[q].x), gxy2[q]);
+            gxy2[q] = __ffma2_rn(make_float2(g.z, g.w), make_float2(cur[q].y, cur[q].y), gxy2[q]);
+          }
         }
         if (POT || (DN && n + 1 < P)) {
           const float4 z = zph[c];
-          gzph = __ffma2_rn(make_float2(z.x, z.y), make_float2(cur.x, cur.x), gzph);
-          gzph = __ffma2_rn(make_float2(z.z, z.w), make_float2(cur.y, cur.y), gzph);
+#pragma unroll
+          for (int q = 0; q < NT; ++q) {
+            gzph[q] = __ffma2_rn(make_float2(z.x, z.y), make_float2(cur[q].x, cur[q].x), gzph[q]);
+            gzph[q] = __ffma2_rn(make_float2(z.z, z.w), make_float2(cur[q].y, cur[q].y), gzph[q]);
+          }
         }
       }
     }
-    if (POT) pot.y[i] += pot.b * gzph.y * inv_w;
-    if (DN) {
-      const float4 nn = nrm[i];
-      dn.y[i] += dn.b * (nn.x * gxy2.x + nn.y * gxy2.y + nn.z * gzph.x) * inv_w * inv_w;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const int i = i0 + 32 * q;
+      if (i >= e) break;
+      if (POT) pot.y[i] += pot.b * gzph[q].y * inv_w;
+      if (DN) {
+        const float4 nn = nrm[i];
+        dn.y[i] += dn.b * (nn.x * gxy2[q].x + nn.y * gxy2[q].y + nn.z * gzph[q].x) * inv_w * inv_w;
+      }
     }
   }
 }

@@ -116,6 +116,7 @@ bool m2m_rot_supported(int P);
 void launch_m2m_rot(fmmbem_ctx* c, int l, const int* scnt, float2* T, cudaStream_t st);
 void launch_l2l_rot(fmmbem_ctx* c, int l, const int* tcnt, cudaStream_t st);
 void scan_ints(const int* in, int* out, int n, cudaStream_t s);  // exclusive
+void scan_i64(const long long* in, long long* out, int n, cudaStream_t s);  // exclusive
 
 // Krylov / reductions
 double dot_weighted(fmmbem_ctx* c, int64_t n, const float* a, const float* b, const float4* w_area,

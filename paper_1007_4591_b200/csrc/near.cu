@@ -125,14 +125,14 @@ __global__ void k_near_count(int nrows, int row0, NearGeom g, int* cnt) {
   cnt[r] = c;
 }
 
-__global__ void k_near_fill(int nrows, int row0, NearGeom g, const int* __restrict__ off, int* col, float* vkp,
+__global__ void k_near_fill(int nrows, int row0, NearGeom g, const long long* __restrict__ off, int* col, float* vkp,
                             float* vsl, float* diag) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
   const int i = row0 + r, p = g.perm[i], leaf = g.leaf[i];
   const double* x = g.cen + 3 * (size_t)p;
   const double* n = g.nrm + 3 * (size_t)p;
-  int w = off[r];
+  long long w = off[r];
   for (int e = g.nbr_off[leaf]; e < g.nbr_off[leaf + 1]; ++e) {
     const int L = g.nbr_idx[e];
     for (int j = g.beg[L]; j < g.beg[L + 1]; ++j) {
@@ -170,15 +170,20 @@ __global__ void k_near_fill(int nrows, int row0, NearGeom g, const int* __restri
 }
 
 // y[i] += b * (sum_k val[k] x[col[k]] + diag[i] x[i]) for the rows [row0, row0 + nrows)
-__global__ void k_near_apply(int nrows, int row0, const int* __restrict__ off, const int* __restrict__ col,
+__global__ void k_near_apply(int nrows, int row0, const long long* __restrict__ off, const int* __restrict__ col,
                              const float* __restrict__ val, const float* __restrict__ diag, const float* __restrict__ x,
                              float* __restrict__ y, float b) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
   const int i = row0 + r;
   float s = diag ? diag[r] * x[i] : 0.f;
-  for (int k = off[r]; k < off[r + 1]; ++k) s = fmaf(val[k], x[col[k]], s);
+  for (long long k = off[r]; k < off[r + 1]; ++k) s = fmaf(val[k], x[col[k]], s);
   y[i] = fmaf(b, s, y[i]);
+}
+
+__global__ void k_widen_near(int n, const int* __restrict__ in, long long* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
 }
 
 __global__ void k_max_sqrt_area(int64_t n, const double* __restrict__ area, unsigned int* out) {
@@ -218,18 +223,21 @@ void build_near(fmmbem_ctx* c, const double* V, const int* T, const double* cen,
   auto& N = c->near;
   N.off.alloc(nrows + 1);
   DevBuf<int> cnt;
+  DevBuf<long long> cnt64;
   cnt.alloc(nrows + 1);
+  cnt64.alloc(nrows + 1);
   cnt.zero(st);
   if (nrows > 0) k_near_count<<<ceil_div(nrows, 128), 128, 0, st>>>(nrows, row0, g, cnt.get());
+  k_widen_near<<<ceil_div(nrows + 1, 256), 256, 0, st>>>(nrows + 1, cnt.get(), cnt64.get());
   FMM_CHECK_LAUNCH();
-  scan_ints(cnt.get(), N.off.get(), nrows + 1, st);
-  int nnz = 0;
-  FMM_CUDA(cudaMemcpyAsync(&nnz, N.off.get() + nrows, sizeof(int), cudaMemcpyDeviceToHost, st));
+  scan_i64(cnt64.get(), N.off.get(), nrows + 1, st);
+  long long nnz = 0;
+  FMM_CUDA(cudaMemcpyAsync(&nnz, N.off.get() + nrows, sizeof(long long), cudaMemcpyDeviceToHost, st));
   FMM_CUDA(cudaStreamSynchronize(st));
   N.nnz = nnz;
-  N.col.alloc(std::max(nnz, 1));
-  N.vkp.alloc(std::max(nnz, 1));
-  N.vsl.alloc(std::max(nnz, 1));
+  N.col.alloc(std::max<long long>(nnz, 1));
+  N.vkp.alloc(std::max<long long>(nnz, 1));
+  N.vsl.alloc(std::max<long long>(nnz, 1));
   N.diag.alloc(std::max(nrows, 1));
   if (nrows > 0)
     k_near_fill<<<ceil_div(nrows, 128), 128, 0, st>>>(nrows, row0, g, N.off.get(), N.col.get(), N.vkp.get(),

@@ -509,6 +509,7 @@ int64_t merge_cells(fmmbem_ctx* c, DevBuf<uint64_t>& ukey, DevBuf<int>& ucnt, in
 }  // namespace
 
 void scan_ints(const int* in, int* out, int n, cudaStream_t s) { exclusive_scan(in, out, n, s); }
+void scan_i64(const long long* in, long long* out, int n, cudaStream_t s) { exclusive_scan(in, out, n, s); }
 
 void build_halo(fmmbem_ctx* c, const std::vector<int>& hgb, DevBuf<float4>& opos, DevBuf<float4>& onrm,
                 DevBuf<float4>& oquad, DevBuf<long long>& ogid, cudaStream_t s);

@@ -1,5 +1,5 @@
 """bench.py's launch count pinned by measurement: the ncu launch list of the bench command
-(`profiles/r2_launches_bench_c5.csv`, every kernel the process launched, in launch order) shows
+(`profiles/r2_final_launches_bench_c5.csv`, every kernel the process launched, in launch order) shows
 exactly launches_per_matvec(L, P) of the library's kernels per device-path A-matvec at C5 (leaf level
 8, P = 13) -- the count the bench line reports as gpu_launches / steps."""
 import csv
@@ -34,7 +34,7 @@ def _launch_sequence(path):
 
 def test_launches_per_matvec_equals_the_ncu_launch_list():
     b = _bench()
-    seq = _launch_sequence(os.path.join(ROOT, "profiles", "r2_launches_bench_c5.csv"))
+    seq = _launch_sequence(os.path.join(ROOT, "profiles", "r2_final_launches_bench_c5.csv"))
     ours = [k for k in seq if k.startswith("k_")]
     starts = [i for i, k in enumerate(ours) if k == "k_p2m_t"]
     groups = [ours[a:b] for a, b in zip(starts, starts[1:])]
