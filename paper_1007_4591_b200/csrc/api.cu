@@ -938,6 +938,7 @@ void matvec_host_pipelined(fmmbem_ctx* c, fmmbem_op op, const float* xh, float* 
     s.leaf_lo = l0;
     s.leaf_hi = l1;
     s.cnt = c->pan_own_cnt.get();
+    s.halo_src = x + own0;  // distributed sources: the P2P weight exponent is taken over all ranks
     tcnt = c->pan_own_cnt.get();
   }
   c->Mx.zero(st);

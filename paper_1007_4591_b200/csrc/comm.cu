@@ -142,6 +142,13 @@ void comm_allreduce_f64_op(fmmbem_ctx* c, double* buf, size_t n, int op, cudaStr
   check(api().allReduce(buf, buf, n, ncclFloat64, o, (ncclComm_t)c->comm, s), "ncclAllReduce");
 }
 
+// element-wise max of `n` uint32 values over the ranks (second: the caller-stream communicator)
+void comm_allreduce_u32_max(fmmbem_ctx* c, unsigned* buf, size_t n, cudaStream_t s, bool second) {
+  if (c->opt.nranks <= 1 || n == 0) return;
+  const ncclComm_t cm = (ncclComm_t)(second && c->comm2 ? c->comm2 : c->comm);
+  check(api().allReduce(buf, buf, n, ncclUint32, ncclMax, cm, s), "ncclAllReduce");
+}
+
 // every rank's `n` int64 values (device) -> all[r * n + k] (device)
 void comm_allgather_i64(fmmbem_ctx* c, const int64_t* mine, int64_t* all, size_t n, cudaStream_t s) {
   check(api().allGather(mine, all, n, ncclInt64, (ncclComm_t)c->comm, s), "ncclAllGather");

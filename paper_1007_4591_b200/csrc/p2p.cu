@@ -487,12 +487,17 @@ const float4* prepare_p2p_sources(fmmbem_ctx* c, const SrcArg& s, cudaStream_t s
   if ((int64_t)c->p2p_src.n < n) c->p2p_src.alloc(n);
   if (c->p2p_wmax.n < 1) c->p2p_wmax.alloc(1);
   FMM_CUDA(cudaMemsetAsync(c->p2p_wmax.get(), 0, sizeof(unsigned), st));
-  if (n > 0) {
+  if (n > 0)
     k_absmax<<<std::min<int64_t>(4 * 148, ceil_div(n, 256)), 256, 0, st>>>(n, s.set->pos.get(), s.x, s.set->div,
                                                                           c->p2p_wmax.get());
+  // several ranks: the normalisation exponent of the WHOLE source vector (max over ranks of the
+  // non-negative float bits), so the scaled coordinates -- and the product -- do not depend on the
+  // partition (a rank-local exponent changes a = sign(w)/sqrt(|w|/2^e) by sqrt 2 and with it the
+  // rounding of the scaled form: 4e-6 relative at 4 ranks on C3)
+  if (c->nranks > 1 && s.halo_src) comm_allreduce_u32_max(c, c->p2p_wmax.get(), 1, st, /*second=*/true);
+  if (n > 0)
     k_scale_src<<<ceil_div(n, 256), 256, 0, st>>>(n, s.set->pos.get(), s.x, s.set->div, c->p2p_wmax.get(),
                                                    c->p2p_src.get());
-  }
   FMM_CHECK_LAUNCH();
   return c->p2p_src.get();
 }

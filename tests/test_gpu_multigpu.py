@@ -2,7 +2,7 @@
 near-field weights, LET multipoles -- reproduces the single-GPU matvec, GMRES solve, BIBEE energy and
 reaction potential, with the full mesh on every rank (input_mode 0) and with every rank passing only
 its part (input_mode 1; also with every triangle on one rank and none on the others), and with the
-self-term / analytic near-field options.  Needs >= 2 GPUs."""
+self-term / analytic near-field options, at 2 ranks and (C3) at 4.  Needs >= 2 / 4 GPUs."""
 import json
 import os
 import subprocess
@@ -25,10 +25,15 @@ def run_check(case, n):
     return json.loads(line[0][5:])
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("case", ["lyso40", "c3"])
-def test_two_gpus_match_one(case):
-    r = run_check(case, 2)
+def _gpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("case,n", [("lyso40", 2), ("c3", 2), ("c3", 4)])
+def test_several_gpus_match_one(case, n):
+    if _gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = run_check(case, n)
     for rk in r["ranks"]:
         for mode in ("mode0", "mode1", "mode2"):
             m = rk[mode]
