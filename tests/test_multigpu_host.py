@@ -221,7 +221,7 @@ def brute_force_check(plans, keys, npan, nchg, L):
             assert ((off[l] + j) in set(plans[0]["shared_chg"])) == (straddle and nchg[ls].sum() > 0)
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_exchange_plan_brute_force_over_gloo(world):
     """fmmbem_plan (the host code fmmbem_create runs on every rank) on a real tree, one process per
     rank over gloo: halo and LET lists agree pairwise and equal the brute-force needs."""
