@@ -460,6 +460,9 @@ def main():
            "e2e": {"value": 1.0 / e2e_s, "unit": "matvec/s", "h2d_bytes_per_step": 4 * n,
                    "d2h_bytes_per_step": 4 * n},
            "comm_ms": ph["comm"],
+           "comm_note": ("CUDA events around the LET exchange on the far-field stream: the interval includes "
+                         "waiting for SMs held by the persistent P2P kernel (DESIGN.md Sec. 11); the step time "
+                         "is the sum of the phases' standalone times") if world > 1 else None,
            "clocks": clocks}
     free, total = torch.cuda.mem_get_info()
     out["device_mem_used_gb"] = (total - free) / 1e9  # this process's device (rank 0 with several)

@@ -858,10 +858,14 @@ void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem
 #ifndef M2L_NREG13
 #define M2L_NREG13 11
 #endif
+#ifndef M2L_NREG12
+#define M2L_NREG12 0
+#endif
 constexpr int m2l_nc(int P) { return P * (P + 1) / 2; }
 constexpr int m2l_warps_for(int P, int nreg) { return (227 * 1024) / ((m2l_nc(P) - nreg) * 33 * 8); }
 constexpr int m2l_nreg(int P) {
   if (P == 13) return M2L_NREG13;
+  if (P == 12 && M2L_NREG12) return M2L_NREG12;
   const int w0 = m2l_warps_for(P, 0);
   for (int k = 1; k <= 4; ++k)
     if (m2l_warps_for(P, k) > w0) return m2l_warps_for(P, k) <= 16 ? k : 0;
