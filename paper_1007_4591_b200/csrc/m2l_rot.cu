@@ -853,13 +853,13 @@ void m2l_sync_launch(const M2LWork& w, const Tree& T, fmmbem_ctx* c, size_t smem
 // lockstep warps per CTA: as many per-warp slots ((NC - NREG) x 33 float2) as fit the SM's 227 KB of
 // shared memory -- one CTA per SM.  NREG = the slot rows kept in registers.  P = 13 (the bench
 // order): 11 rows -> 11 warps instead of 9, 168 registers, no spills (C5: M2L 36.6 -> 33.2 ms; 3 rows
-// / 10 warps: 35.3 ms).  Other orders: the fewest rows (<= 4) that gain one warp while the CTA stays
-// <= 16 warps (>= 128 registers per thread), else none.
+// / 10 warps: 35.3 ms); P = 12: 5 rows -> 12 warps.  Other orders: the fewest rows (<= 4) that gain
+// one warp while the CTA stays <= 16 warps (>= 128 registers per thread), else none.
 #ifndef M2L_NREG13
 #define M2L_NREG13 11
 #endif
 #ifndef M2L_NREG12
-#define M2L_NREG12 0
+#define M2L_NREG12 5  // P = 12 (the charge-FMM order of the bench): 12 warps, M2L 27.2 -> 26.5 ms (13 warps: 28.9)
 #endif
 constexpr int m2l_nc(int P) { return P * (P + 1) / 2; }
 constexpr int m2l_warps_for(int P, int nreg) { return (227 * 1024) / ((m2l_nc(P) - nreg) * 33 * 8); }
