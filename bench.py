@@ -255,6 +255,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1024, help="oracle sample rows for cpu_baseline/parity")
     ap.add_argument("--bibee-calls", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-solve", action="store_true", help="skip the full GMRES solve reported beside the bench line")
     ap.add_argument("--near-mode", type=int, default=0, help="1: analytic flat-panel near field (option a11)")
     ap.add_argument("--charge-terms", type=int, default=None,
                     help="order of the charge-FMM (BIBEE leg); default 12 under K' order 13 (E_n within 1e-4)")
@@ -384,6 +385,23 @@ def main():
                  "energies_per_s": 1e3 / bms,
                  "charge_fmm_phases_ms": {k: float(np.mean([b[k] for b in bph])) for k in bph[0]}}
 
+    # one full BEM solve at this size (GMRES iterations, Delta G): GMRES(30) to
+    # 1e-6 from a zero guess on the cached charge fields, device time of the solve (CUDA events)
+    gm = None
+    if not cube and s.n_charges and not args.no_solve:
+        torch.cuda.synchronize()
+        r = s.solve()
+        tg = s.timing()
+        gms = float(tg["gmres"])
+        if dist:
+            t = torch.tensor([gms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            gms = float(t.item())
+        gm = {"iterations": int(r["iterations"]), "converged": bool(r["converged"]),
+              "rel_residual": float(r["rel_residual"]), "dG_internal": r["dG"], "dG_kcal_mol": r["dG_kcal"],
+              "ms": gms, "ms_per_iteration": gms / max(1, int(r["iterations"])), "tol": 1e-6, "restart": 30}
+        del r
+
     p2p_int = int(tm["p2p_interactions"])
     p2p_s = ph["p2p"] * 1e-3
     if dist:  # job-wide P2P rate: all ranks' interactions over the slowest rank's P2P time
@@ -455,6 +473,7 @@ def main():
            "setup_s": setup_s,
            "tree_build_ms": tm["tree"],
            "bibee_cfa": bibee,
+           "gmres_solve": gm,
            "roofline": roof, "roofline_kernels": kern, "hbm_peak_source": hbm_src,
            "gpu_launches": args.steps * launches_per_matvec(info["levels"], P, info if world > 1 else None),
            "e2e": {"value": 1.0 / e2e_s, "unit": "matvec/s", "h2d_bytes_per_step": 4 * n,

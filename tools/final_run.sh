@@ -9,9 +9,9 @@ timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/fin_gputest.log 2>&1;
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin_smoke.log 2>&1; tail -1 gpurun_out/fin_smoke.log
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/fin_bench.json 2> gpurun_out/fin_bench.err; tail -c 300 gpurun_out/fin_bench.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/fin_bench_ref.json 2> gpurun_out/fin_bench_ref.err; tail -c 300 gpurun_out/fin_bench_ref.json
-timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --bibee-calls 1 > gpurun_out/fin_b_plain.json 2>&1 && \
+timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --bibee-calls 1 --no-solve > gpurun_out/fin_b_plain.json 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fin_launches_bench.csv \
-      python bench.py --steps 2 --warmup 3 --no-cpu --bibee-calls 1 > gpurun_out/fin_ncu_bench.log 2>&1
+      python bench.py --steps 2 --warmup 3 --no-cpu --bibee-calls 1 --no-solve > gpurun_out/fin_ncu_bench.log 2>&1
 timeout 300 python tools/prof_run.py --reps 2 > gpurun_out/fin_prof_plain.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on \
       -k regex:"k_p2p|k_m2l_rot|k_m2m_rot|k_l2l_rot|k_p2m_t|k_l2p_t|k_m2m_sum" -s 22 -c 22 \
