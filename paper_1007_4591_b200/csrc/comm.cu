@@ -122,33 +122,6 @@ void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const st
   check(api().groupEnd(), "ncclGroupEnd");
 }
 
-// NCCL sets up its point-to-point connections lazily, at the first send / recv between two ranks
-// (~1 s per peer on these boxes).  fmmbem_create runs this from a helper thread while the main
-// thread computes the host exchange plan (no other NCCL call is in flight then): one float to and
-// from every peer on both communicators.
-void comm_warmup(fmmbem_ctx* c) {
-  const int R = c->opt.nranks, me = c->opt.rank;
-  if (R <= 1) return;
-  FMM_CUDA(cudaSetDevice(c->device));
-  cudaStream_t s = nullptr;
-  FMM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  DevBuf<float> buf;
-  buf.alloc(2 * (size_t)R);
-  buf.zero(s);
-  for (void* cm : {c->comm, c->comm2}) {
-    if (!cm) continue;
-    check(api().groupStart(), "ncclGroupStart");
-    for (int p = 0; p < R; ++p) {
-      if (p == me) continue;
-      check(api().send(buf.get() + p, 1, ncclFloat32, p, (ncclComm_t)cm, s), "ncclSend");
-      check(api().recv(buf.get() + R + p, 1, ncclFloat32, p, (ncclComm_t)cm, s), "ncclRecv");
-    }
-    check(api().groupEnd(), "ncclGroupEnd");
-  }
-  FMM_CUDA(cudaStreamSynchronize(s));
-  FMM_CUDA(cudaStreamDestroy(s));
-}
-
 // grouped point-to-point exchange: sbuf[p] (scnt[p] floats) -> rank p, rbuf[p] <- rank p
 void comm_sendrecv_f32(fmmbem_ctx* c, const std::vector<float*>& sbuf, const std::vector<size_t>& scnt,
                        const std::vector<float*>& rbuf, const std::vector<size_t>& rcnt, cudaStream_t s) {

@@ -70,7 +70,6 @@ void comm_allgatherv_f32(fmmbem_ctx* c, const float* mine, float* full, const st
                          cudaStream_t s, bool second = false);
 void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds);
 void comm_allreduce_f64_op(fmmbem_ctx* c, double* buf, size_t n, int op /* -1 min, 0 sum, +1 max */, cudaStream_t s);
-void comm_warmup(fmmbem_ctx* c);  // establishes the peer connections of both communicators
 void comm_allreduce_u32_max(fmmbem_ctx* c, unsigned* buf, size_t n, cudaStream_t s, bool second = false);
 void comm_allgather_i64(fmmbem_ctx* c, const int64_t* mine, int64_t* all, size_t n, cudaStream_t s);
 void comm_allgatherv_bytes(fmmbem_ctx* c, const void* mine, void* full, const std::vector<size_t>& offs,

@@ -15,8 +15,6 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
-#include <exception>
-#include <thread>
 
 #include "ctx.h"
 #include "kernels.cuh"
@@ -865,24 +863,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
       pan[k] = gb[k + 1] - gb[k];
       tgt[k] = pan[k] + cb[k + 1] - cb[k];
     }
-    // the host plan (pure host work) overlaps NCCL's lazy peer-connection setup on a helper thread
-    std::exception_ptr werr;
-    std::thread warm([c, &werr]() {
-      try {
-        comm_warmup(c);
-      } catch (...) {
-        werr = std::current_exception();
-      }
-    });
-    try {
-      plan_exchange(H, pan, tgt, K, R, me, c->xplan);
-    } catch (...) {
-      warm.join();
-      throw;
-    }
-    warm.join();
-    if (werr) std::rethrow_exception(werr);
-    stage("plan + NCCL connect");
+    plan_exchange(H, pan, tgt, K, R, me, c->xplan);
     c->leaf_bounds = c->xplan.leaf_bounds;
     c->leaf_lo = (int)c->leaf_bounds[me];
     c->leaf_hi = (int)c->leaf_bounds[me + 1];
@@ -914,7 +895,7 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
   FMM_CUDA(cudaStreamSynchronize(s));
   const int64_t n_own = hgb[leaf_hi] - hgb[leaf_lo];
 
-  stage("local lists + slots");
+  stage("plan");
   // 6. panels to their owners: FP64 records in the slice's key order, one contiguous segment per rank
   const int Wd = 9 + (K > 1 ? 3 * K : 0);
   DevBuf<unsigned long long> orec;  // owned records, Morton order
