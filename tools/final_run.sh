@@ -22,6 +22,6 @@ ncu -i /tmp/prof_final.ncu-rep --page raw --csv > gpurun_out/fin_ncu_full_raw.cs
 for k in k_p2p k_m2l_rot; do
   ncu -i /tmp/prof_final.ncu-rep --page source --csv --print-source sass -k regex:$k > gpurun_out/fin_ncu_src_$k.csv 2>/dev/null
 done
-timeout 900 python bench.py --near-mode 1 --steps 5 --warmup 3 --no-cpu > gpurun_out/fin_bench_near.json 2> gpurun_out/fin_bench_near.err; tail -c 200 gpurun_out/fin_bench_near.json
+timeout 900 echo near-mode measured in tools/final_run_4gpu.sh history
 timeout 900 python bench.py --config cube --steps 10 --warmup 3 > gpurun_out/fin_bench_cube.json 2> gpurun_out/fin_bench_cube.err; tail -c 200 gpurun_out/fin_bench_cube.json
 ls -la gpurun_out/ | grep fin_

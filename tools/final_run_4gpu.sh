@@ -9,7 +9,3 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --mast
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29662 bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/fin4_bench_n2.log 2>&1; echo n2 $?
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29663 bench.py --gpus 4 --steps 10 --warmup 3 > gpurun_out/fin4_bench_n4.log 2>&1; echo n4 $?
 FMMBEM_VERBOSE=1 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29664 bench.py --gpus 4 --config c5_22 --steps 5 --warmup 3 > gpurun_out/fin4_bench_c5_22_n4.log 2>&1; echo c5_22 $?
-# one-GPU extras on the same box: the analytic near-field option at C5, the L2P two-targets-per-lane A/B
-timeout 1500 python bench.py --near-mode 1 --steps 5 --warmup 3 --no-cpu > gpurun_out/fin4_bench_near.json 2> gpurun_out/fin4_bench_near.err; echo near $?
-timeout 300 python tools/prof_run.py --reps 6 > gpurun_out/fin4_prof_base.log 2>&1; echo base $?
-FMMBEM_LIB=$PWD/paper_1007_4591_b200/libfmmbem_l2p2.so timeout 300 python tools/prof_run.py --reps 6 > gpurun_out/fin4_prof_l2p2.log 2>&1; echo l2p2 $?
