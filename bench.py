@@ -386,10 +386,12 @@ def main():
                  "charge_fmm_phases_ms": {k: float(np.mean([b[k] for b in bph])) for k in bph[0]}}
 
     # one full BEM solve at this size (GMRES iterations, Delta G): GMRES(30) to
-    # 1e-6 from a zero guess on the cached charge fields, device time of the solve (CUDA events)
+    # 1e-6 from a zero guess on the cached charge fields, device time of the solve (CUDA events);
+    # the second of two solves (the first allocates the Krylov basis)
     gm = None
     if not cube and s.n_charges and not args.no_solve:
         torch.cuda.synchronize()
+        s.solve()  # warm-up: allocates the basis
         r = s.solve()
         tg = s.timing()
         gms = float(tg["gmres"])

@@ -457,9 +457,11 @@ void ensure_fields(fmmbem_ctx* c, cudaStream_t st) {
     FMM_CHECK_LAUNCH();
     FMM_CUDA(cudaStreamSynchronize(st));
   }
-  int flag = 0;
-  FMM_CUDA(cudaMemcpyAsync(&flag, c->flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
-  FMM_CUDA(cudaStreamSynchronize(st));
+  int flag = 0;  // only the checked evaluation can raise it: later calls stay asynchronous
+  if (check) {
+    FMM_CUDA(cudaMemcpyAsync(&flag, c->flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMM_CUDA(cudaStreamSynchronize(st));
+  }
   if (check && multi(c)) {  // the verdict is collective: every rank throws or none does
     double f = flag ? 1.0 : 0.0;
     c->red.alloc(std::max<size_t>(c->red.n, 64));
@@ -1038,12 +1040,11 @@ fmmbem_status fmmbem_bibee_energy(fmmbem_ctx* c, fmmbem_bibee v, float* sig, fmm
   const double s = (v == FMMBEM_BIBEE_CFA) ? -0.5 : (v == FMMBEM_BIBEE_P ? 0.0 : 0.5);
   const double d = 1.0 - c->f * s;
   if (d == 0.0) throw Error(FMMBEM_E_INVALID, "1 - f s == 0 (SPEC S:383)");
-  DevBuf<float> tmp;
   const int64_t n = c->n_own();
   float* sh = sig;
-  if (!sh) {
-    tmp.alloc(std::max<int64_t>(n, 1));
-    sh = tmp.get();
+  if (!sh) {  // ctx scratch, allocated once (an allocation here would stall the timed interval)
+    c->tmp_y.alloc(std::max<int64_t>(std::max<int64_t>(n, 1), (int64_t)c->tmp_y.n));
+    sh = c->tmp_y.get();
   }
   // sigma_hat = f E / (1 - f s)   (Eq. 7 with K' -> s I, reading A3)
   if (n > 0) k_scale<<<ceil_div(n, 256), 256, 0, st>>>(sh, c->En.get(), n, (float)(c->f / d));
