@@ -15,7 +15,11 @@
 // (ABI, host only) builds the skeleton lists here first, so tests can check the plan on a CPU.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <thread>
 #include <string>
 #include <vector>
@@ -102,115 +106,173 @@ void host_tree(const uint64_t* leaf_keys, int64_t nl, int L, HostTree& T) {
   }
 }
 
+// [0, n) split over nth host threads: f(lo, hi, thread)
+template <class F>
+void parallel_for(int64_t n, int nth, F f) {
+  nth = (int)std::max<int64_t>(1, std::min<int64_t>(nth, n / 4096));
+  if (nth <= 1) {
+    f((int64_t)0, n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nth; ++t) th.emplace_back(f, n * t / nth, n * (t + 1) / nth, t);
+  for (auto& t : th) t.join();
+}
+
 // Partition + halo + LET (see the file header).  leaf_pan / leaf_tgt: panels / target points
 // (panels + charges) per leaf of all ranks; K: quadrature points per panel (P2P sources).
+// Every loop is split over the host threads a rank may use (hardware threads / ranks, <= 16);
+// the results do not depend on the split.
 void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int K,
                    int R, int me, ExchangePlan& X) {
+  static const bool verbose = std::getenv("FMMBEM_VERBOSE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!verbose) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[fmmbem plan %d] %-14s %8.1f ms\n", me, what,
+                 std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
+  const int nth = (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency() / (unsigned)std::max(1, R)));
   const int L = T.L;
   const int64_t nl = T.lvl_off[L + 1] - T.lvl_off[L], nc = T.lvl_off[L + 1];
   const int64_t leaf0 = T.lvl_off[L];
   // leaf cost: P2P interactions + M2L translations (~600 interaction-equivalents each) + per point
   std::vector<double> cost(nl);
-  for (int64_t k = 0; k < nl; ++k) {
-    long long s = 0;
-    for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1]; ++e) s += leaf_pan[T.nbr_idx[e]];
-    const long long nt = leaf_pan[k];
-    const double m2l = (double)(T.m2l_off[leaf0 + k + 1] - T.m2l_off[leaf0 + k]);
-    cost[k] = (double)(nt * s * K) + (nt ? 600.0 * m2l : 0.0) + 50.0 * (double)nt;
-  }
+  parallel_for(nl, nth, [&](int64_t lo_k, int64_t hi_k, int) {
+    for (int64_t k = lo_k; k < hi_k; ++k) {
+      long long s = 0;
+      for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1]; ++e) s += leaf_pan[T.nbr_idx[e]];
+      const long long nt = leaf_pan[k];
+      const double m2l = (double)(T.m2l_off[leaf0 + k + 1] - T.m2l_off[leaf0 + k]);
+      cost[k] = (double)(nt * s * K) + (nt ? 600.0 * m2l : 0.0) + 50.0 * (double)nt;
+    }
+  });
   X.leaf_bounds.assign(R + 1, 0);
   split_costs(cost.data(), nl, R, X.leaf_bounds.data());
+  stage("cost+split");
   std::vector<int> lrank(nl);
   for (int r = 0; r < R; ++r)
     for (int64_t k = X.leaf_bounds[r]; k < X.leaf_bounds[r + 1]; ++k) lrank[k] = r;
-  const int lo = (int)X.leaf_bounds[me], hi = (int)X.leaf_bounds[me + 1];
-  // near-field halo
+  // near-field halo: per-thread chunks of leaves, concatenated in leaf order
   X.halo_send.assign(R, {});
   X.halo_recv.assign(R, {});
-  for (int64_t k = 0; k < nl; ++k) {
-    if (lrank[k] == me) {
-      unsigned long long m = 0;
-      for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1]; ++e) m |= 1ULL << lrank[T.nbr_idx[e]];
-      for (int p = 0; p < R; ++p)
-        if (p != me && (m >> p & 1ULL)) X.halo_send[p].push_back((int)k);
-    } else {
-      bool need = false;
-      for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1] && !need; ++e) need = lrank[T.nbr_idx[e]] == me;
-      if (need) X.halo_recv[lrank[k]].push_back((int)k);
-    }
+  {
+    std::vector<std::vector<std::vector<int>>> hs(nth, std::vector<std::vector<int>>(R)), hr(hs);
+    parallel_for(nl, nth, [&](int64_t lo_k, int64_t hi_k, int t) {
+      for (int64_t k = lo_k; k < hi_k; ++k) {
+        if (lrank[k] == me) {
+          unsigned long long m = 0;
+          for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1]; ++e) m |= 1ULL << lrank[T.nbr_idx[e]];
+          for (int p = 0; p < R; ++p)
+            if (p != me && (m >> p & 1ULL)) hs[t][p].push_back((int)k);
+        } else {
+          bool need = false;
+          for (int e = T.nbr_off[k]; e < T.nbr_off[k + 1] && !need; ++e) need = lrank[T.nbr_idx[e]] == me;
+          if (need) hr[t][lrank[k]].push_back((int)k);
+        }
+      }
+    });
+    for (int t = 0; t < nth; ++t)
+      for (int p = 0; p < R; ++p) {
+        X.halo_send[p].insert(X.halo_send[p].end(), hs[t][p].begin(), hs[t][p].end());
+        X.halo_recv[p].insert(X.halo_recv[p].end(), hr[t][p].begin(), hr[t][p].end());
+      }
   }
-  (void)lo;
-  (void)hi;
-  // local essential tree: leaf range and owner of every cell (levels >= 2), sources per cell.
-  // Panel multipoles serve every target point (K', V, A at panels; the reaction potential at the
-  // charges); charge multipoles serve the panels (E_n, psi of the charge-FMM).
+  stage("halo");
+  // local essential tree: leaf range [first, end) and owner of every cell (levels >= 2), sources
+  // per cell.  Panel multipoles serve every target point (K', V, A at panels; the reaction
+  // potential at the charges); charge multipoles serve the panels (E_n, psi of the charge-FMM).
   std::vector<long long> tpre(nl + 1, 0), ppre(nl + 1, 0);
   for (int64_t k = 0; k < nl; ++k) {
     tpre[k + 1] = tpre[k] + leaf_tgt[k];
     ppre[k + 1] = ppre[k] + leaf_pan[k];
   }
-  const int64_t c0 = T.lvl_off[std::min(2, L + 1)];
+  const int c0l = std::min(2, L + 1);
+  const int64_t c0 = T.lvl_off[c0l];
   std::vector<int> first(nc, 0), end(nc, 0), owner(nc, -1);
   std::vector<char> has_src(nc, 0), has_chg(nc, 0);
-  for (int64_t c = c0; c < nc; ++c) {
-    int l = 0;
-    while (c >= T.lvl_off[l + 1]) ++l;
+  std::vector<unsigned long long> tmask(nc, 0), pmask(nc, 0);  // ranks with targets / panels below
+  for (int l = c0l; l <= L; ++l) {  // the cells of a level and the leaves are both key-sorted: one sweep
     const int sh = 3 * (L - l);
-    const uint64_t a = T.key[c] << sh, b = (T.key[c] + 1) << sh;
-    first[c] = lower_bound_key(T.key, leaf0, T.lvl_off[L + 1], a) - (int)leaf0;
-    end[c] = lower_bound_key(T.key, leaf0, T.lvl_off[L + 1], b) - (int)leaf0;
-    if (end[c] > first[c] && lrank[first[c]] == lrank[end[c] - 1]) owner[c] = lrank[first[c]];
-    has_src[c] = ppre[end[c]] > ppre[first[c]];
-    has_chg[c] = (tpre[end[c]] - tpre[first[c]]) > (ppre[end[c]] - ppre[first[c]]);
+    int64_t j = 0;
+    for (int64_t c = T.lvl_off[l]; c < T.lvl_off[l + 1]; ++c) {
+      while (j < nl && (T.key[leaf0 + j] >> sh) < T.key[c]) ++j;
+      first[c] = (int)j;
+      while (j < nl && (T.key[leaf0 + j] >> sh) == T.key[c]) ++j;
+      end[c] = (int)j;
+    }
   }
+  parallel_for(nc - c0, nth, [&](int64_t lo_i, int64_t hi_i, int) {
+    for (int64_t c = c0 + lo_i; c < c0 + hi_i; ++c) {
+      if (end[c] <= first[c]) continue;
+      if (lrank[first[c]] == lrank[end[c] - 1]) owner[c] = lrank[first[c]];
+      has_src[c] = ppre[end[c]] > ppre[first[c]];
+      has_chg[c] = (tpre[end[c]] - tpre[first[c]]) > (ppre[end[c]] - ppre[first[c]]);
+      unsigned long long tm = 0, pm = 0;
+      for (int p = lrank[first[c]]; p <= lrank[end[c] - 1]; ++p) {
+        const int f = std::max(first[c], (int)X.leaf_bounds[p]), e = std::min(end[c], (int)X.leaf_bounds[p + 1]);
+        if (e > f && tpre[e] > tpre[f]) tm |= 1ULL << p;
+        if (e > f && ppre[e] > ppre[f]) pm |= 1ULL << p;
+      }
+      tmask[c] = tm;
+      pmask[c] = pm;
+    }
+  });
+  stage("cell ranges");
+  // Which pure cells move: the interaction lists are symmetric (s in list(c) <=> c in list(s): the
+  // parents are neighbours, the cells are not), so the ranks that need a pure cell s (targets below
+  // some c whose list holds s) are the OR of tmask over s's OWN list.  Each rank evaluates that for
+  // the cells it owns (to send) and for the cells of the lists of the cells holding its targets (to
+  // receive) -- about 2/R of one pass over all lists, no atomics.
   X.let_send.assign(R, {});
   X.let_recv.assign(R, {});
   X.let_shared.clear();
   X.let_send_chg.assign(R, {});
   X.let_recv_chg.assign(R, {});
   X.let_shared_chg.clear();
-  // one pass over the interaction lists: need[s] = ranks holding targets below some cell whose list
-  // contains s (rank-bit masks; set-if-missing atomics, so the lists are split over host threads)
-  std::vector<std::atomic<unsigned long long>> need(nc), need_c(nc);
-  for (auto& v : need) v.store(0, std::memory_order_relaxed);
-  for (auto& v : need_c) v.store(0, std::memory_order_relaxed);
-  auto work = [&](int64_t lo_c, int64_t hi_c) {
-    for (int64_t c = lo_c; c < hi_c; ++c) {
-      if (end[c] <= first[c]) continue;
-      unsigned long long tm = 0, pm = 0;  // ranks with target points / panels below c
-      for (int p = lrank[first[c]]; p <= lrank[end[c] - 1]; ++p) {
-        const int f = std::max(first[c], (int)X.leaf_bounds[p]), e = std::min(end[c], (int)X.leaf_bounds[p + 1]);
-        if (e > f && tpre[e] > tpre[f]) tm |= 1ULL << p;
-        if (e > f && ppre[e] > ppre[f]) pm |= 1ULL << p;
+  std::vector<unsigned long long> need(nc, 0), need_c(nc, 0);
+  // the cells this rank sends: the OR of tmask / pmask over their own lists
+  parallel_for(nc - c0, nth, [&](int64_t lo_i, int64_t hi_i, int) {
+    for (int64_t s_ = c0 + lo_i; s_ < c0 + hi_i; ++s_) {
+      if (owner[s_] != me || !(has_src[s_] || has_chg[s_])) continue;
+      unsigned long long m = 0, mc = 0;
+      for (int64_t k = T.m2l_off[s_]; k < T.m2l_off[s_ + 1]; ++k) {
+        m |= tmask[T.m2l_idx[k]];
+        mc |= pmask[T.m2l_idx[k]];
       }
-      if (!tm) continue;
-      for (int64_t k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k) {
-        const int sidx = T.m2l_idx[k];
-        if (has_src[sidx]) {
-          auto& v = need[sidx];
-          if ((v.load(std::memory_order_relaxed) & tm) != tm) v.fetch_or(tm, std::memory_order_relaxed);
-        }
-        if (pm && has_chg[sidx]) {
-          auto& v = need_c[sidx];
-          if ((v.load(std::memory_order_relaxed) & pm) != pm) v.fetch_or(pm, std::memory_order_relaxed);
-        }
-      }
+      need[s_] = has_src[s_] ? m : 0;
+      need_c[s_] = has_chg[s_] ? mc : 0;
     }
-  };
-  const int64_t ncell = nc - c0;
-  int nth = (int)std::max(1u, std::thread::hardware_concurrency() / (unsigned)std::max(1, R));
-  nth = (int)std::min<int64_t>(std::min(nth, 16), std::max<int64_t>(1, ncell / 65536));
-  if (nth <= 1) {
-    work(c0, nc);
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nth; ++t) th.emplace_back(work, c0 + ncell * t / nth, c0 + ncell * (t + 1) / nth);
-    for (auto& t : th) t.join();
+  });
+  // the cells this rank receives: those in the lists of the cells holding its targets / panels
+  {
+    std::unique_ptr<std::atomic<unsigned char>[]> flag(new std::atomic<unsigned char>[nc]);
+    for (int64_t c = 0; c < nc; ++c) flag[c].store(0, std::memory_order_relaxed);
+    const unsigned long long bit = 1ULL << me;
+    parallel_for(nc - c0, nth, [&](int64_t lo_i, int64_t hi_i, int) {
+      for (int64_t c = c0 + lo_i; c < c0 + hi_i; ++c) {
+        const bool t = tmask[c] & bit, p = pmask[c] & bit;
+        if (!t) continue;
+        for (int64_t k = T.m2l_off[c]; k < T.m2l_off[c + 1]; ++k) {
+          const int s_ = T.m2l_idx[k];
+          if (owner[s_] < 0 || owner[s_] == me) continue;
+          const unsigned char f = (has_src[s_] ? 1 : 0) | ((p && has_chg[s_]) ? 2 : 0);
+          if (f && (flag[s_].load(std::memory_order_relaxed) & f) != f) flag[s_].fetch_or(f, std::memory_order_relaxed);
+        }
+      }
+    });
+    for (int64_t c = c0; c < nc; ++c) {
+      const unsigned char f = flag[c].load(std::memory_order_relaxed);
+      if (f & 1) need[c] |= bit;
+      if (f & 2) need_c[c] |= bit;
+    }
   }
-  auto lists = [&](const std::vector<char>& has, const std::vector<std::atomic<unsigned long long>>& nd,
+  auto lists = [&](const std::vector<char>& has, const std::vector<unsigned long long>& nd,
                    std::vector<std::vector<int>>& snd, std::vector<std::vector<int>>& rcv, std::vector<int>& shr) {
     for (int64_t c = c0; c < nc; ++c) {
-      const unsigned long long m = nd[c].load(std::memory_order_relaxed);
+      const unsigned long long m = nd[c];
       if (owner[c] < 0) {
         if (has[c]) shr.push_back((int)c);
         continue;
@@ -223,9 +285,12 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
       }
     }
   };
+  stage("need pass");
   lists(has_src, need, X.let_send, X.let_recv, X.let_shared);
   lists(has_chg, need_c, X.let_send_chg, X.let_recv_chg, X.let_shared_chg);
+  stage("LET lists");
   slot_layout(T, me, X);
+  stage("slots");
 }
 
 // Windows of this rank's cells per level and the slot numbering (plan.h).  A cell of level l holds
