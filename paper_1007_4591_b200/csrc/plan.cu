@@ -30,7 +30,7 @@ namespace fmm {
 
 namespace {
 
-int lower_bound_key(const std::vector<uint64_t>& a, int64_t lo, int64_t hi, uint64_t v) {
+int lower_bound_key(const HostVec<uint64_t>& a, int64_t lo, int64_t hi, uint64_t v) {
   return (int)(std::lower_bound(a.begin() + lo, a.begin() + hi, v) - a.begin());
 }
 

@@ -2,22 +2,47 @@
 #pragma once
 #include <stdint.h>
 
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
 
 namespace fmm {
 
+// std::vector whose resize() leaves new elements uninitialised (the host copies of the device
+// lists are overwritten by cudaMemcpy right away: zeroing 10 GB at 1e9 panels costs seconds)
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using HostVec = std::vector<T, NoInitAlloc<T>>;
+
 // The octree skeleton on the host: cells of every level (level-major, sorted keys), child ranges,
 // leaf neighbour lists (leaf indices) and interaction lists (global cell indices).
 struct HostTree {
   int L = 0;
   std::vector<int64_t> lvl_off;
-  std::vector<uint64_t> key;
+  HostVec<uint64_t> key;
   std::vector<int> child_b, child_e;
-  std::vector<int> nbr_off, nbr_idx;
-  std::vector<int64_t> m2l_off;
-  std::vector<int> m2l_idx;
+  HostVec<int> nbr_off, nbr_idx;
+  HostVec<int64_t> m2l_off;
+  HostVec<int> m2l_idx;
 };
 
 struct ExchangePlan {
