@@ -123,20 +123,22 @@ void parallel_for(int64_t n, int nth, F f) {
 // (panels + charges) per leaf of all ranks; K: quadrature points per panel (P2P sources).
 // Every loop is split over the host threads a rank may use (hardware threads / ranks, <= 16);
 // the results do not depend on the split.
-void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int K,
-                   int R, int me, ExchangePlan& X) {
-  static const bool verbose = std::getenv("FMMBEM_VERBOSE") != nullptr;
-  auto t_last = std::chrono::steady_clock::now();
-  auto stage = [&](const char* what) {
-    if (!verbose) return;
-    const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[fmmbem plan %d] %-14s %8.1f ms\n", me, what,
-                 std::chrono::duration<double, std::milli>(t - t_last).count());
-    t_last = t;
-  };
-  const int nth = (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency() / (unsigned)std::max(1, R)));
+namespace {
+bool plan_verbose() {
+  static const bool v = std::getenv("FMMBEM_VERBOSE") != nullptr;
+  return v;
+}
+int plan_threads(int R) {
+  return (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency() / (unsigned)std::max(1, R)));
+}
+}  // namespace
+
+// the cost-weighted contiguous leaf partition (needs only the neighbour lists and the per-leaf
+// interaction-list lengths: fmmbem_create calls it before copying any interaction list to the host)
+void plan_partition(const HostTree& T, const std::vector<int>& leaf_pan, int K, int R, ExchangePlan& X) {
+  const int nth = plan_threads(R);
   const int L = T.L;
-  const int64_t nl = T.lvl_off[L + 1] - T.lvl_off[L], nc = T.lvl_off[L + 1];
+  const int64_t nl = T.lvl_off[L + 1] - T.lvl_off[L];
   const int64_t leaf0 = T.lvl_off[L];
   // leaf cost: P2P interactions + M2L translations (~600 interaction-equivalents each) + per point
   std::vector<double> cost(nl);
@@ -151,7 +153,31 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
   });
   X.leaf_bounds.assign(R + 1, 0);
   split_costs(cost.data(), nl, R, X.leaf_bounds.data());
-  stage("cost+split");
+}
+
+void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int K,
+                   int R, int me, ExchangePlan& X) {
+  plan_partition(T, leaf_pan, K, R, X);
+  plan_lists(T, leaf_pan, leaf_tgt, R, me, X);
+}
+
+// Halo, LET and slots for the partition in X.leaf_bounds.  Reads the interaction lists of this
+// rank's window cells only (the cells it owns and the cells holding its targets), so fmmbem_create
+// passes a tree whose lists outside the windows are empty.
+void plan_lists(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int R, int me,
+                ExchangePlan& X) {
+  auto t_last = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!plan_verbose()) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[fmmbem plan %d] %-14s %8.1f ms\n", me, what,
+                 std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
+  const int nth = plan_threads(R);
+  const int L = T.L;
+  const int64_t nl = T.lvl_off[L + 1] - T.lvl_off[L], nc = T.lvl_off[L + 1];
+  const int64_t leaf0 = T.lvl_off[L];
   std::vector<int> lrank(nl);
   for (int r = 0; r < R; ++r)
     for (int64_t k = X.leaf_bounds[r]; k < X.leaf_bounds[r + 1]; ++k) lrank[k] = r;
@@ -295,15 +321,13 @@ void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const st
 
 // Windows of this rank's cells per level and the slot numbering (plan.h).  A cell of level l holds
 // a leaf of [lo, hi) iff its key lies between the level-l ancestors of leaves lo and hi - 1.
-void slot_layout(const HostTree& T, int me, ExchangePlan& X) {
+void plan_windows(const HostTree& T, int me, ExchangePlan& X) {
   const int L = T.L;
   const int64_t leaf0 = T.lvl_off[L];
   const int64_t lo = X.leaf_bounds[me], hi = X.leaf_bounds[me + 1];
   X.lvl_off = T.lvl_off;
   X.win_lo.assign(L + 1, 0);
   X.win_hi.assign(L + 1, 0);
-  X.slot_base.assign(L + 1, 0);
-  int64_t n = 0;
   for (int l = 0; l <= L; ++l) {
     X.win_lo[l] = X.win_hi[l] = T.lvl_off[l];
     if (hi > lo) {
@@ -311,6 +335,15 @@ void slot_layout(const HostTree& T, int me, ExchangePlan& X) {
       X.win_lo[l] = lower_bound_key(T.key, T.lvl_off[l], T.lvl_off[l + 1], T.key[leaf0 + lo] >> sh);
       X.win_hi[l] = lower_bound_key(T.key, T.lvl_off[l], T.lvl_off[l + 1], T.key[leaf0 + hi - 1] >> sh) + 1;
     }
+  }
+}
+
+void slot_layout(const HostTree& T, int me, ExchangePlan& X) {
+  const int L = T.L;
+  plan_windows(T, me, X);
+  X.slot_base.assign(L + 1, 0);
+  int64_t n = 0;
+  for (int l = 0; l <= L; ++l) {
     X.slot_base[l] = n;
     n += X.win_hi[l] - X.win_lo[l];
   }

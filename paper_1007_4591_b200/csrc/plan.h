@@ -64,7 +64,11 @@ struct ExchangePlan {
 
 void host_tree(const uint64_t* leaf_keys, int64_t nl, int L, HostTree& T);
 void plan_exchange(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int K,
-                   int R, int me, ExchangePlan& X);
+                   int R, int me, ExchangePlan& X);  // = plan_partition + plan_lists
+void plan_partition(const HostTree& T, const std::vector<int>& leaf_pan, int K, int R, ExchangePlan& X);
+void plan_lists(const HostTree& T, const std::vector<int>& leaf_pan, const std::vector<int>& leaf_tgt, int R, int me,
+                ExchangePlan& X);
+void plan_windows(const HostTree& T, int me, ExchangePlan& X);  // win_lo / win_hi of X.leaf_bounds[me..]
 void slot_layout(const HostTree& T, int me, ExchangePlan& X);  // windows + extra cells (plan_exchange calls it)
 void split_costs(const double* cost, int64_t n, int parts, int64_t* bounds);
 

@@ -848,13 +848,11 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
     H.nbr_off.resize(nl + 1);
     H.nbr_idx.resize(T.nbr_pairs);
     H.m2l_off.resize(T.n_cells + 1);
-    H.m2l_idx.resize(T.m2l_pairs);
     std::vector<int> gb(nl + 1), cb(nl + 1);
     FMM_CUDA(cudaMemcpyAsync(H.key.data(), T.key.get(), T.n_cells * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(H.nbr_off.data(), T.nbr_off.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(H.nbr_idx.data(), T.nbr_idx.get(), T.nbr_pairs * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(H.m2l_off.data(), T.m2l_off.get(), (T.n_cells + 1) * sizeof(long long), cudaMemcpyDeviceToHost, s));
-    FMM_CUDA(cudaMemcpyAsync(H.m2l_idx.data(), T.m2l_idx.get(), T.m2l_pairs * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(gb.data(), c->gbeg.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaMemcpyAsync(cb.data(), C.begin.get(), (nl + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaStreamSynchronize(s));
@@ -863,7 +861,34 @@ void build_tree(fmmbem_ctx* c, const PanelInput& in, const double* wq, const dou
       pan[k] = gb[k + 1] - gb[k];
       tgt[k] = pan[k] + cb[k + 1] - cb[k];
     }
-    plan_exchange(H, pan, tgt, K, R, me, c->xplan);
+    // the partition needs only the list lengths; the rest of the plan reads the lists of this
+    // rank's window cells, so only those come to the host (~1/R of 10 GB at 1e9 panels)
+    plan_partition(H, pan, K, R, c->xplan);
+    plan_windows(H, me, c->xplan);
+    {
+      const ExchangePlan& X = c->xplan;
+      HostVec<int64_t> full = std::move(H.m2l_off);
+      H.m2l_off.resize(T.n_cells + 1);
+      int64_t pos = 0;
+      std::vector<int64_t> seg_dst(L + 1, 0);
+      for (int l = 0; l <= L; ++l) {
+        const int64_t wlo = X.win_lo[l], whi = X.win_hi[l], base = full[wlo];
+        seg_dst[l] = pos;
+        for (int64_t cc = T.lvl_off[l]; cc < T.lvl_off[l + 1]; ++cc)
+          H.m2l_off[cc] = pos + (cc < wlo ? 0 : (cc < whi ? full[cc] - base : full[whi] - base));
+        pos += full[whi] - base;
+      }
+      H.m2l_off[T.n_cells] = pos;
+      H.m2l_idx.resize(std::max<int64_t>(pos, 1));
+      for (int l = 0; l <= L; ++l) {
+        const int64_t a = full[X.win_lo[l]], b = full[X.win_hi[l]];
+        if (b > a)
+          FMM_CUDA(cudaMemcpyAsync(H.m2l_idx.data() + seg_dst[l], T.m2l_idx.get() + a, (b - a) * sizeof(int),
+                                   cudaMemcpyDeviceToHost, s));
+      }
+      FMM_CUDA(cudaStreamSynchronize(s));
+    }
+    plan_lists(H, pan, tgt, R, me, c->xplan);
     c->leaf_bounds = c->xplan.leaf_bounds;
     c->leaf_lo = (int)c->leaf_bounds[me];
     c->leaf_hi = (int)c->leaf_bounds[me + 1];
