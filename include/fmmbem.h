@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define FMMBEM_ABI_VERSION 2
+#define FMMBEM_ABI_VERSION 3  /* 3: options.charge_terms, tree_info expansion slots / LET counts, plan lists 10-14 */
 
 typedef struct fmmbem_ctx fmmbem_ctx; /* opaque */
 

@@ -62,7 +62,7 @@ class TreeInfo(C.Structure):
 
 
 # symbol -> (restype, argtypes); every entry point declared in include/fmmbem.h
-ABI_VERSION = 2  # include/fmmbem.h FMMBEM_ABI_VERSION this binding is written for
+ABI_VERSION = 3  # include/fmmbem.h FMMBEM_ABI_VERSION this binding is written for
 
 SIGNATURES = {
     "fmmbem_abi_version": (C.c_int32, []),
