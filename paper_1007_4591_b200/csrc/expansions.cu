@@ -107,8 +107,14 @@ __device__ __forceinline__ void p2m_columns(float2 (&acc)[p2m_half(P)], float2* 
 // memory once (u = (y - c)/w, weight) with their starting diagonals (R_0^0 = 1, R_H^H), then every
 // lane accumulates its sources' columns in registers (two columns at a time for ILP) and the column
 // pair is reduced over the lanes at once, so shared memory stays small (occupancy) whatever P.
+// 28 resident blocks: 72 registers (32 B of spills), P2M 6.31 -> 6.10 ms at C5 (1: 104 registers,
+// 7.5 ms; plain bounds: 80 registers, 6.3 ms; 32: 64 registers + 116 B spills, 6.3 ms)
+#ifndef P2M_MINB
+#define P2M_MINB 28
+#endif
+#define P2M_BOUNDS __launch_bounds__(32, P2M_MINB)
 template <int P>
-__global__ void __launch_bounds__(32) k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
+__global__ void P2M_BOUNDS k_p2m_t(const float4* __restrict__ pos, const float* __restrict__ x, int div,
                                               const int* __restrict__ beg, float inv_w, int leaf_off, int leaf0,
                                               float2* __restrict__ M) {
   constexpr int NC = P * (P + 1) / 2;
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(32) k_l2p_t(const float4* __restrict__ pos, co
     }
 #pragma unroll
     for (int m = 0; m < P; ++m) {
-      asm volatile("" ::: "memory");  // re-read the tables per column (no hoisting over the target loop)
+      asm volatile("" ::: "memory");  // re-read the tables per column (without: 168 registers, 1.1 KB spills)
       float2 cur[NT], prev[NT];
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
